@@ -1,0 +1,193 @@
+/* scd.h — C ABI of the B200-native TPA-SCD library (paper_1702_07005_b200/libscd.so).
+ *
+ * Hot path of Parnell, Dünner, Atasu, Sifalakis, Pozidis, "Large-Scale Stochastic Learning
+ * using GPUs" (arXiv 1702.07005): the twice-parallel asynchronous stochastic coordinate
+ * descent (TPA-SCD) epoch for L2-regularised ridge regression, in the primal form (by
+ * feature, CSC columns) and the dual form (SDCA, by example, CSR rows), the fp64 objective and
+ * duality-gap evaluation, and the distributed aggregation with add / average / closed-form
+ * optimal gamma.  Citations: "P:n" = PAPER.md line n, with the section / equation /
+ * algorithm it belongs to.  Readings of ambiguous passages are DESIGN.md §4 items (cN).
+ *
+ * Problem (§II): A ∈ R^{N×M} (N examples, M features), y ∈ R^N, λ > 0.
+ *   primal  P(β) = 1/(2N)||Aβ - y||² + λ/2 ||β||²                 Eq. (1)
+ *   dual    D(α) = -N/2 ||α||² - 1/(2λ)||Aᵀα||² + αᵀy             Eq. (3)
+ *
+ * Conventions for every entry point:
+ *  - Every call returns scd_status; nothing throws or aborts across the ABI.  On failure a
+ *    context-owned message is available from scd_last_error(ctx) (valid until the next call
+ *    on that context); context-free calls report through scd_last_global_error().
+ *  - Data is fp32 (values, labels, model, shared vector) with int32 inner indices and int64
+ *    outer offsets ("all data is represented using 32-bit floating point").  Objective,
+ *    gap and gamma are computed and returned in fp64.
+ *  - "device" pointers are CUDA device pointers on the current device at scd_create time.
+ *  - Calls on one context are not thread-safe; distinct contexts may be used concurrently.
+ *  - scd_epoch only enqueues work on the context stream (no host sync).  scd_objective,
+ *    scd_duality_gap, scd_aggregate, scd_get_* synchronise that stream.
+ */
+#ifndef SCD_H
+#define SCD_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SCD_OK = 0,
+  SCD_E_INVALID_ARG = 1,  /* λ <= 0, N < 1, M < 1, null pointer, length mismatch, form/layout mismatch */
+  SCD_E_BAD_MATRIX = 2,   /* offsets/indices violate the CSR/CSC invariants; scd_last_error names the first bad outer index */
+  SCD_E_OOM = 3,          /* device allocation failed */
+  SCD_E_CUDA = 4,         /* a CUDA runtime call or kernel failed */
+  SCD_E_NCCL = 5,         /* an NCCL call failed */
+  SCD_E_STATE = 6,        /* call not valid in the context's state (e.g. world > 1 without a communicator) */
+  SCD_E_UNSUPPORTED = 7   /* valid request this build does not implement */
+} scd_status;
+
+typedef enum { SCD_PRIMAL = 0 /* A must be CSC (by feature) */, SCD_DUAL = 1 /* A must be CSR (by example) */ } scd_form;
+
+/* Aggregation of the K workers' updates each round (§IV): γ = 1 (adding), γ = 1/K
+ * (averaging, Alg. 3), or the closed-form optimum (Alg. 4, Eq. 7 P:362 and the dual γ̄
+ * P:369, with the corrections of DESIGN.md c3, c4, c5). */
+typedef enum { SCD_AGG_ADD = 0, SCD_AGG_AVERAGE = 1, SCD_AGG_OPTIMAL = 2 } scd_agg;
+
+typedef enum { SCD_MEM_HOST = 0, SCD_MEM_DEVICE = 1 } scd_mem;
+typedef enum { SCD_CSR = 0, SCD_CSC = 1 } scd_layout;
+
+/* Sparse matrix (the local shard of A).  outer = n_rows for CSR, n_cols for CSC.
+ *   ptr[outer+1]: ptr[0] = 0, nondecreasing, ptr[outer] = nnz
+ *   idx[nnz]    : inner indices in [0, inner), strictly increasing within each outer index
+ *   val[nnz]    : values (NULL is rejected in this build: SCD_E_UNSUPPORTED)
+ * Ownership: if mem == SCD_MEM_DEVICE the arrays are BORROWED for the lifetime of the context
+ * (the caller keeps them alive and unmodified until scd_destroy; the paper's data "is
+ * transferred into the GPU memory once ... and does not move").  If SCD_MEM_HOST the
+ * library copies them to the device during scd_create and owns the copy.                    */
+typedef struct {
+  scd_layout layout;
+  int64_t n_rows, n_cols, nnz;
+  const int64_t *ptr;
+  const int32_t *idx;
+  const float *val;
+  scd_mem mem;
+} scd_matrix;
+
+typedef struct {
+  uint64_t seed;          /* permutation key: epoch t visits coordinates in P_t = feistel(seed, t) order (c8) */
+  int64_t n_global;       /* N used in λN when the dual is sharded by example (c14); 0 = n_rows */
+  int32_t rank, world;    /* world = K workers; 1 = single GPU (default) */
+  void *nccl_comm;        /* ncclComm_t, required iff world > 1 (see scd_nccl_comm_init); not owned */
+  void *stream;           /* cudaStream_t for all work; NULL = a context-owned stream */
+  int32_t deterministic;  /* 1 = debug mode: ONE coordinate at a time in exact P_t order, fixed reduction
+                             tree; bitwise repeatable (parity with the sequential oracle, Alg. 1) */
+  int32_t max_inflight;   /* cap on coordinates in flight in the asynchronous kernels; 0 = auto */
+  int32_t recompute_every;/* rebuild the shared vector from the model every k epochs; 0 = off */
+  int32_t validate;       /* 1 = check the matrix invariants on the device at create (default 1) */
+  int32_t profile;        /* 1 = time every kernel launch of scd_epoch with CUDA events (scd_profile_read) */
+} scd_options;
+
+typedef struct scd_ctx scd_ctx;
+
+/* Fills *opt with defaults: seed 0, n_global 0, rank 0, world 1, no comm, NULL stream,
+ * deterministic 0, max_inflight 0 (auto), recompute_every 0, validate 1, profile 0. */
+void scd_default_options(scd_options *opt);
+
+/* Creates a solver context for the ridge problem (A, y, λ) in the given form.
+ *   A     : local shard, CSC for SCD_PRIMAL (N × M_k: all rows, own columns), CSR for SCD_DUAL
+ *           (N_k × M: own rows, all columns).
+ *   y     : labels, length A->n_rows (dual: the shard's rows); copied if y_mem == SCD_MEM_HOST,
+ *           borrowed if SCD_MEM_DEVICE.
+ *   lambda: λ > 0.
+ * Initial state: model = 0, shared vector = 0 (w = Aβ = 0; w̄ = Aᵀα = 0), as in Alg. 1/2
+ * "Initialize: β = 0, w = 0".  Precomputes the squared norms ||a_m||² / ||ā_n||²
+ * (c9) and the coordinate schedule.  Errors: SCD_E_INVALID_ARG, SCD_E_BAD_MATRIX, SCD_E_OOM,
+ * SCD_E_CUDA, SCD_E_STATE (world > 1 without nccl_comm).  On error *out is NULL.            */
+scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double lambda, scd_form form,
+                      const scd_options *opt, scd_ctx **out);
+
+/* One local epoch (Alg. 2): every local coordinate is updated exactly once, in the
+ * order P_epoch, by the rule Eq. (2) (primal) or Eq. (4) (dual); the shared vector
+ * is updated with fp32 atomic adds.  Asynchronous: many coordinates in flight
+ * (any interleaving is a valid execution, c19) unless options.deterministic.  Enqueued on the
+ * context stream; returns without synchronising.                                               */
+scd_status scd_epoch(scd_ctx *c, uint32_t epoch);
+
+/* Primal and dual objectives, fp64, computed from scratch (the shared vector is NOT trusted).
+ *   primal form: *primal = P(β), *dual = D((y - Aβ)/N)      (Eq. 6 map)
+ *   dual form  : *primal = P(Aᵀα/λ), *dual = D(α)            (Eq. 5 map)
+ * Collective over the workers if world > 1.  Either output pointer may be NULL.  Syncs.     */
+scd_status scd_objective(scd_ctx *c, double *primal, double *dual);
+
+/* Duality gap G_P(β) / G_D(α) of §II.C, fp64, from scratch, evaluated through the
+ * cancellation-free identity G_P = ||∇P(β)||²/(2λ), G_D = ||∇D(α)||²/(2N) (c13).  Collective
+ * if world > 1.  Syncs.                                                                       */
+scd_status scd_duality_gap(scd_ctx *c, double *gap);
+
+/* One aggregation round of Alg. 3/4 over the world's workers, after each ran
+ * scd_epoch from the common base point: Δ_k = (local state) - (base), Δw = Σ_k Δw_k (NCCL
+ * all-reduce over NVLink when world > 1), γ per mode, then w = w_base + γΔw and
+ * model_k = model_k,base + γΔmodel_k; the result becomes the next base point (c6).
+ * *gamma (may be NULL) receives γ.  A zero update gives γ = 0 for SCD_AGG_OPTIMAL (c16).
+ * Collective if world > 1.  Syncs.                                                            */
+scd_status scd_aggregate(scd_ctx *c, scd_agg mode, double *gamma);
+
+/* The same round for k logical workers living on ONE device (each ctx created with world = 1
+ * and its own shard; all on the same device, same form and λ, n_global = the total N for the
+ * dual).  Used to test the distributed algorithm without a multi-GPU box.  Syncs.            */
+scd_status scd_aggregate_group(scd_ctx *const *ctxs, int32_t k, scd_agg mode, double *gamma);
+
+/* Copies β_k (primal, length n_cols) or α_k (dual, length n_rows) to host memory. Syncs. */
+scd_status scd_get_model(scd_ctx *c, float *host_out, int64_t len);
+/* Copies the shared vector w = Aβ (primal, length N) or w̄ = Aᵀα (dual, length M) to host.
+ * (Internally the primal keeps the residual r = y - w; w is formed on the device.)  Syncs.   */
+scd_status scd_get_shared(scd_ctx *c, float *host_out, int64_t len);
+/* Sets the model from host memory and rebuilds the shared vector from it (fp64 accumulate;
+ * collective if world > 1); resets the aggregation base point.  Syncs.                      */
+scd_status scd_set_model(scd_ctx *c, const float *host_in, int64_t len);
+/* Rebuilds the shared vector from the model (the recomputation scheme of A-SCD). Syncs. */
+scd_status scd_recompute_shared(scd_ctx *c);
+
+/* The cudaStream_t the context enqueues on. */
+scd_status scd_get_stream(scd_ctx *c, void **stream);
+
+typedef struct {
+  int64_t n_coord;        /* local coordinates (M_k primal, N_k dual) */
+  int64_t n_shared;       /* shared-vector length (N primal, M dual) */
+  int64_t nnz;
+  int64_t n_nonempty;     /* coordinates with at least one stored entry */
+  int32_t n_bins;         /* asynchronous schedule: number of coordinate bins (one kernel launch each) */
+  int32_t bin_kind[4];    /* per bin: lanes per coordinate (4..32 = sub-warp group, >= 64 = whole CTA) */
+  int64_t bin_count[4];   /* coordinates per bin */
+  int64_t bin_nnz[4];     /* stored entries per bin */
+  int32_t bin_grid[4];    /* CTAs launched per bin */
+  int32_t bin_block[4];   /* threads per CTA per bin */
+  int64_t launches;       /* kernels launched by scd_epoch since create (cumulative) */
+} scd_info;
+scd_status scd_get_info(scd_ctx *c, scd_info *info);
+
+/* Per-kernel CUDA-event timing of scd_epoch launches (options.profile = 1): for each bin b,
+ * ms_out[b] = summed device time of its launches since the last read, count_out[b] = launches.
+ * Synchronises.  n = capacity of the arrays (>= 4 recommended); returns the bins filled.     */
+scd_status scd_profile_read(scd_ctx *c, double *ms_out, int64_t *count_out, int32_t n, int32_t *filled);
+
+const char *scd_last_error(const scd_ctx *c);   /* context-owned, valid until the next call on c */
+const char *scd_last_global_error(void);         /* thread-local, for context-free calls */
+const char *scd_status_string(scd_status s);
+void scd_destroy(scd_ctx *c);                    /* NULL-safe; syncs the stream; frees owned memory */
+
+/* ---- integer artefacts (computed on the device; bit-exact with the oracle) ---- */
+/* host_out[j] = P_(seed,epoch,stream)(j) for j in [0, n): the keyed Feistel bijection of c8. */
+scd_status scd_permutation(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *host_out);
+/* owner_out[c] (host) = worker owning coordinate c in [0, count) for k workers (c15). */
+scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_owner_out);
+/* Stable transpose CSR <-> CSC computed on the device.  in->mem says where the input lives;
+ * out_mem where ptr_out[inner+1] / idx_out[nnz] / val_out[nnz] (caller-allocated) live.
+ * Within each output outer index, entries appear in increasing input-outer order.           */
+scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out, scd_mem out_mem);
+
+/* ---- NCCL bootstrap helpers (the caller broadcasts the 128-byte id, e.g. via torch.distributed) ---- */
+scd_status scd_nccl_unique_id(void *id_out_128);
+scd_status scd_nccl_comm_init(const void *id_128, int32_t world, int32_t rank, void **comm_out);
+scd_status scd_nccl_comm_destroy(void *comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCD_H */
