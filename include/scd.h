@@ -158,7 +158,10 @@ typedef struct {
   int64_t bin_nnz[4];     /* stored entries per bin */
   int32_t bin_grid[4];    /* CTAs launched per bin */
   int32_t bin_block[4];   /* threads per CTA per bin */
-  int64_t launches;       /* kernels launched by scd_epoch since create (cumulative) */
+  int64_t launches;       /* kernels launched by the context since create (cumulative) */
+  double tau_star;        /* estimated staleness bound: coordinates in flight before the asynchronous
+                             step stops being contractive */
+  int64_t inflight_cap;   /* coordinates in flight actually allowed (max_inflight or tau_star/2) */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

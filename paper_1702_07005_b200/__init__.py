@@ -1,0 +1,12 @@
+"""B200-native TPA-SCD (Parnell et al., arXiv 1702.07005): ridge regression by twice-parallel
+asynchronous stochastic coordinate descent, primal (CSC) and dual (CSR), with fp64 objective /
+duality-gap evaluation and distributed add / average / optimal-gamma aggregation over NCCL.
+
+The compute lives in ``libscd.so`` (hand-written sm_100a CUDA behind the C ABI of
+``include/scd.h``); ``scd`` is the ctypes binding with the same names.
+"""
+from .scd import (AGG, ScdError, Solver, aggregate_group, lib, nccl_comm_destroy, nccl_comm_init,  # noqa: F401
+                  nccl_unique_id, partition, permutation, transpose)
+
+__all__ = ["Solver", "aggregate_group", "permutation", "partition", "transpose", "nccl_unique_id",
+           "nccl_comm_init", "nccl_comm_destroy", "ScdError", "AGG", "lib"]

@@ -1,0 +1,212 @@
+// common.cuh — internal declarations of libscd (B200 TPA-SCD).  Not part of the ABI.
+// P:n = PAPER.md line n.  Readings cN = DESIGN.md §4.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "scd.h"
+
+namespace scd {
+
+constexpr int kMaxBins = 4;
+constexpr uint32_t kPartStream = 0x50415254u;  // "PART": partition permutation stream (c15)
+
+// ------------------------------------------------------------------------------------------
+// Keyed Feistel permutation P_(seed,epoch,stream) on [0, n) (Alg. 1 "Generate random
+// permutation" P:144 / Alg. 2; generator fixed by reading c8).  4-round balanced Feistel
+// on [0, 4^h), h = ceil(ceil(log2 n)/2), with cycle-walking into [0, n): a bijection computed
+// inline per coordinate (no permutation array is stored or read).
+// ------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+struct Perm {
+  uint64_t k0, k1, k2, k3;  // round keys
+  uint64_t n;
+  uint64_t mask;
+  int h;
+};
+
+inline Perm make_perm(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n) {
+  Perm p;
+  uint64_t key = mix64(seed ^ mix64(((uint64_t)epoch << 32) | (uint64_t)stream));
+  p.k0 = mix64(key + 0);
+  p.k1 = mix64(key + 1);
+  p.k2 = mix64(key + 2);
+  p.k3 = mix64(key + 3);
+  p.n = (uint64_t)(n > 0 ? n : 0);
+  int bits = 0;
+  uint64_t v = (n >= 2) ? (uint64_t)(n - 1) : 0;
+  while (v) { ++bits; v >>= 1; }
+  p.h = (bits + 1) / 2;
+  p.mask = (p.h >= 32) ? 0xFFFFFFFFull : ((1ull << p.h) - 1ull);
+  return p;
+}
+
+__device__ __forceinline__ uint64_t feistel_round(uint64_t x, const Perm &p) {
+  uint64_t L = x >> p.h, R = x & p.mask, t;
+  t = L ^ (mix64(R ^ p.k0) & p.mask); L = R; R = t;
+  t = L ^ (mix64(R ^ p.k1) & p.mask); L = R; R = t;
+  t = L ^ (mix64(R ^ p.k2) & p.mask); L = R; R = t;
+  t = L ^ (mix64(R ^ p.k3) & p.mask); L = R; R = t;
+  return (L << p.h) | R;
+}
+
+__device__ __forceinline__ uint64_t perm_apply(const Perm &p, uint64_t j) {
+  if (p.n <= 1) return 0;
+  uint64_t x = j;
+  do { x = feistel_round(x, p); } while (x >= p.n);
+  return x;
+}
+
+// ------------------------------------------------------------------------------------------
+// Context
+// ------------------------------------------------------------------------------------------
+struct Bin {
+  int lanes = 0;             // lanes per coordinate: 8 / 32 (sub-warp group) or blockDim (CTA)
+  int64_t count = 0, nnz = 0;
+  int32_t *list = nullptr;   // device, coordinate ids ascending
+  int grid = 0, block = 0;
+  uint32_t stream_id = 0;    // permutation stream = 1 + bin index
+  double ms = 0.0;           // profiling accumulator
+  int64_t prof_launches = 0;
+};
+
+}  // namespace scd
+
+struct scd_ctx {
+  scd_form form;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int64_t n_coord = 0, n_shared = 0;
+  double lam = 0, lamN = 0;
+  int64_t n_global = 0;
+  scd_options opt{};
+  int device = 0, nsm = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // matrix (device) — borrowed or owned
+  const int64_t *ptr = nullptr;
+  const int32_t *idx = nullptr;
+  const float *val = nullptr;
+  void *own_ptr = nullptr, *own_idx = nullptr, *own_val = nullptr;
+  const float *y = nullptr;  // labels [n_rows]
+  void *own_y = nullptr;
+  // model and shared vector (fp32) plus aggregation base point snapshots
+  float *x = nullptr, *x0 = nullptr;    // β (primal) / α (dual)  [n_coord]
+  float *sv = nullptr, *sv0 = nullptr;  // r = y - Aβ (primal) / w̄ = Aᵀα (dual)  [n_shared]
+  float *norm = nullptr;                // ||a_m||² / ||ā_n||²  [n_coord]
+  // asynchronous schedule
+  int n_bins = 0;
+  scd::Bin bins[scd::kMaxBins];
+  int32_t *empty_list = nullptr;
+  int64_t n_empty = 0, n_nonempty = 0;
+  bool empty_dirty = true;
+  unsigned int *counters = nullptr;  // [kMaxBins] ticket counters
+  // scratch
+  double *acc = nullptr;    // [32] fp64 accumulators (objective / gap / gamma)
+  double *vec64 = nullptr;  // [n_shared] fp64 (u = Aβ or v = Aᵀα)
+  float *comm = nullptr;    // [n_shared] fp32 aggregation buffer (Δ of the shared vector)
+  ncclComm_t nccl = nullptr;
+  // profiling
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+  int64_t launches = 0;
+  uint32_t epochs_done = 0;
+  double tau_star = 0.0;   // estimated staleness bound (coordinates in flight), layout.cu
+  int64_t auto_cap = 0;    // default max coordinates in flight = tau_star / 2
+  std::string err;
+};
+
+namespace scd {
+
+// error helpers -------------------------------------------------------------------------------
+scd_status fail(scd_ctx *c, scd_status s, const std::string &msg);
+scd_status cuda_fail(scd_ctx *c, cudaError_t e, const char *what);
+void set_global_error(const std::string &msg);
+
+#define SCD_CK(ctx, call)                                  \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return scd::cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+#define SCD_CKL(ctx, what)                                 \
+  do {                                                     \
+    cudaError_t e_ = cudaGetLastError();                   \
+    if (e_ != cudaSuccess) return scd::cuda_fail(ctx, e_, what); \
+  } while (0)
+
+#define SCD_NCK(ctx, call)                                 \
+  do {                                                     \
+    ncclResult_t r_ = (call);                              \
+    if (r_ != ncclSuccess) return scd::fail(ctx, SCD_E_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// layout.cu ------------------------------------------------------------------------------------
+scd_status validate_matrix(scd_ctx *c, int64_t outer, int64_t inner);
+scd_status compute_norms(scd_ctx *c);
+scd_status build_schedule(scd_ctx *c);
+scd_status estimate_inflight_cap(scd_ctx *c);
+scd_status transpose_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
+                            int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, cudaStream_t s, std::string &err);
+
+// epoch.cu -------------------------------------------------------------------------------------
+scd_status run_epoch(scd_ctx *c, uint32_t epoch);
+scd_status profile_collect(scd_ctx *c);
+void bin_launch_shape(scd_ctx *c, Bin &b);
+scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
+scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);
+
+// evaluate.cu ----------------------------------------------------------------------------------
+scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap);
+scd_status rebuild_shared(scd_ctx *c);
+scd_status shared_to_w(scd_ctx *c, float *d_out);
+
+// aggregate.cu ---------------------------------------------------------------------------------
+scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma);
+scd_status aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, double *gamma);
+
+// shared device helpers ------------------------------------------------------------------------
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide fp64 sum of `v` added atomically into *out (one atomic per block).
+template <int T>
+__device__ __forceinline__ void block_sum_atomic(double v, double *out) {
+  __shared__ double s_part[T / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_part[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = (lane < T / 32) ? s_part[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) atomicAdd(out, t);
+  }
+  __syncthreads();
+}
+
+inline int grid_for(int64_t n, int block, int cap = 148 * 16) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace scd

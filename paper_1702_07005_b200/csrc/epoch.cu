@@ -1,0 +1,404 @@
+// epoch.cu — the TPA-SCD epoch kernels (Alg. 2) for sm_100a.
+//
+// One epoch updates every local coordinate exactly once, in the order of the epoch
+// permutation, by the closed-form rule
+//   primal (CSC, Eq. 2):  Δβ_m = (<y - w, a_m> - λNβ_m) / (||a_m||² + λN)
+//   dual   (CSR, Eq. 4): Δα_n = (λy_n - <w̄, ā_n> - λNα_n) / (λN + ||ā_n||²)
+// followed by the shared-vector update w += a_m Δβ / w̄ += ā_n Δα written with
+// fp32 atomic adds ("floating point atomic additions", Alg. 2).  The primal keeps
+// the residual r = y - w instead of w, so the gather reads one vector (design note).
+//
+// Kernels:
+//   k_epoch_cta<FORM,T,E>    one coordinate per CTA (the paper's "thread block per coordinate",
+//                            P:190), persistent grid with a global ticket counter; each thread
+//                            keeps E entries of the coordinate in registers between the gather-dot
+//                            and the scatter (no HBM re-read), longer coordinates stream extra chunks.
+//   k_epoch_group<FORM,G,E>  one coordinate per G-lane sub-warp group (short coordinates: a whole
+//                            CTA would idle), warp-shuffle reduction, E entries per lane in registers.
+//   k_epoch_debug<FORM>      deterministic mode: one CTA, one coordinate at a time in exact P_t
+//                            order, fixed reduction tree -> bitwise repeatable (oracle parity).
+//   k_empty_fix<FORM>        coordinates with no stored entry: Δ = -β_m (primal) / y_n/N - α_n (dual)
+//                            (c17); only re-run when the model was set externally.
+#include "common.cuh"
+
+namespace scd {
+namespace {
+
+struct EpochArgs {
+  const int64_t *__restrict__ ptr;
+  const int32_t *__restrict__ idx;
+  const float *__restrict__ val;
+  const float *__restrict__ y;
+  const float *__restrict__ norm;
+  float *x;
+  float *sv;
+  double lam, lamN;
+};
+
+struct BinArgs {
+  const int32_t *list;  // coordinate ids of the bin (ascending); nullptr = identity
+  int64_t count;
+  unsigned int *counter;
+  Perm perm;
+};
+
+// Closed-form coordinate delta (Eq. 2 / Eq. 4), scalar math in fp64 (free), result fp32.
+template <int FORM>
+__device__ __forceinline__ float coord_delta(float dp, float xc, float nrm, float yc, double lam, double lamN) {
+  double num = (FORM == SCD_PRIMAL) ? ((double)dp - lamN * (double)xc)
+                                    : (lam * (double)yc - (double)dp - lamN * (double)xc);
+  return (float)(num / ((double)nrm + lamN));
+}
+// primal scatters into r = y - w (so -Δ), dual into w̄ (+Δ)
+template <int FORM>
+__device__ __forceinline__ float scatter_scale(float d) { return FORM == SCD_PRIMAL ? -d : d; }
+
+// Shared-vector gather: L2-coherent load (bypasses L1) so a hot entry is never served stale
+// from L1 while other SMs' atomics land in L2.
+__device__ __forceinline__ float ld_sv(const float *p) { return __ldcg(p); }
+__device__ __forceinline__ void red_add(float *p, float v) { atomicAdd(p, v); }  // RED.E.ADD.F32
+
+__device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
+  uint64_t j = perm_apply(b.perm, t);
+  return b.list ? (int64_t)__ldg(b.list + j) : (int64_t)j;
+}
+
+// ----------------------------------------------------------------------------------------------
+template <int FORM, int T, int E>
+__global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
+  constexpr int NW = T / 32;
+  __shared__ float s_red[NW];
+  __shared__ float s_delta;
+  __shared__ unsigned int s_ticket;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (;;) {
+    if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
+    __syncthreads();
+    const unsigned int t = s_ticket;
+    if (t >= (uint64_t)b.count) break;
+    const int64_t c = bin_coord(b, t);
+    const int64_t beg = __ldg(a.ptr + c), end = __ldg(a.ptr + c + 1);
+    int32_t id[E];
+    float v[E];
+    float acc = 0.f;
+    // first chunk: held in registers until the scatter
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = beg + (int64_t)e * T + tid;
+      if (k < end) {
+        id[e] = __ldcs(a.idx + k);
+        v[e] = __ldcs(a.val + k);
+      } else {
+        id[e] = -1;
+        v[e] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
+    // remaining chunks of a long coordinate (re-read for the scatter; L2-resident by then)
+    for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
+#pragma unroll 4
+      for (int e = 0; e < E; ++e) {
+        const int64_t k = base + (int64_t)e * T + tid;
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+      float s = lane < NW ? s_red[lane] : 0.f;
+      s = warp_sum(s);
+      if (lane == 0) {
+        const float xc = a.x[c];
+        const float d = coord_delta<FORM>(s, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f,
+                                          a.lam, a.lamN);
+        a.x[c] = xc + d;  // single writer per epoch (c10)
+        s_delta = d;
+      }
+    }
+    __syncthreads();
+    const float d = scatter_scale<FORM>(s_delta);
+    if (d != 0.f) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
+      for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
+#pragma unroll 4
+        for (int e = 0; e < E; ++e) {
+          const int64_t k = base + (int64_t)e * T + tid;
+          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
+template <int FORM, int G, int E>
+__global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
+  constexpr int CPW = 32 / G;  // coordinates per warp per ticket
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / G, gl = lane % G;
+  for (;;) {
+    unsigned int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(b.counter, (unsigned)CPW);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if (t0 >= (uint64_t)b.count) break;  // warp-uniform
+    // lanes 0..CPW-1 evaluate the permutation for the warp's CPW tickets, then broadcast
+    int64_t cl = -1;
+    if (lane < CPW && t0 + lane < (uint64_t)b.count) cl = bin_coord(b, t0 + lane);
+    const int64_t c = __shfl_sync(0xffffffffu, cl, sub);
+    const bool active = c >= 0;
+    int64_t beg = 0, end = 0;
+    if (active) {
+      beg = __ldg(a.ptr + c);
+      end = __ldg(a.ptr + c + 1);
+    }
+    int32_t id[E];
+    float v[E];
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = beg + (int64_t)e * G + gl;
+      if (k < end) {
+        id[e] = __ldcs(a.idx + k);
+        v[e] = __ldcs(a.val + k);
+      } else {
+        id[e] = -1;
+        v[e] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
+    for (int64_t base = beg + (int64_t)G * E; base < end; base += (int64_t)G * E) {
+#pragma unroll 4
+      for (int e = 0; e < E; ++e) {
+        const int64_t k = base + (int64_t)e * G + gl;
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    float d = 0.f;
+    if (active && gl == 0) {  // group leader: single writer of x[c] (c10)
+      const float xc = a.x[c];
+      d = coord_delta<FORM>(acc, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f, a.lam, a.lamN);
+      a.x[c] = xc + d;
+    }
+    d = scatter_scale<FORM>(__shfl_sync(0xffffffffu, d, sub * G));
+    if (d != 0.f) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
+      for (int64_t base = beg + (int64_t)G * E; base < end; base += (int64_t)G * E) {
+#pragma unroll 4
+        for (int e = 0; e < E; ++e) {
+          const int64_t k = base + (int64_t)e * G + gl;
+          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Deterministic (debug) epoch: exactly Alg. 1's order with Alg. 2's arithmetic, one coordinate
+// at a time, fixed reduction tree (strided per-thread partials -> xor-shuffle tree -> 8 warp
+// partials summed in order).  Plain read-modify-write scatter: one coordinate in flight and
+// unique indices within a coordinate, so there is no race.
+constexpr int kDbgT = 256;
+template <int FORM>
+__global__ void __launch_bounds__(kDbgT) k_epoch_debug(EpochArgs a, Perm perm, int64_t n) {
+  __shared__ float s_red[kDbgT / 32];
+  __shared__ float s_delta;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t c = (int64_t)perm_apply(perm, (uint64_t)j);
+    const int64_t beg = a.ptr[c], end = a.ptr[c + 1];
+    float acc = 0.f;
+    for (int64_t k = beg + tid; k < end; k += kDbgT) acc = fmaf(a.sv[a.idx[k]], a.val[k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[wid] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      float s = 0.f;
+      for (int w = 0; w < kDbgT / 32; ++w) s += s_red[w];
+      const float xc = a.x[c];
+      const float d = coord_delta<FORM>(s, xc, a.norm[c], FORM == SCD_DUAL ? a.y[c] : 0.f, a.lam, a.lamN);
+      a.x[c] = xc + d;
+      s_delta = d;
+    }
+    __syncthreads();
+    const float d = scatter_scale<FORM>(s_delta);
+    for (int64_t k = beg + tid; k < end; k += kDbgT) a.sv[a.idx[k]] += a.val[k] * d;
+    __syncthreads();
+  }
+}
+
+template <int FORM>
+__global__ void k_empty_fix(EpochArgs a, const int32_t *list, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = list[i];
+    const float xc = a.x[c];
+    a.x[c] = xc + coord_delta<FORM>(0.f, xc, 0.f, FORM == SCD_DUAL ? a.y[c] : 0.f, a.lam, a.lamN);
+  }
+}
+
+__global__ void k_perm_export(Perm p, int64_t n, int64_t *out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = (int64_t)perm_apply(p, (uint64_t)j);
+}
+
+__global__ void k_partition_export(Perm p, int64_t count, int32_t k, int32_t *owner) {
+  const int64_t base = count / k, rem = count % k;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = (int64_t)perm_apply(p, (uint64_t)i);
+    const int64_t blk = (i < rem * (base + 1)) ? i / (base + 1) : rem + (i - rem * (base + 1)) / base;
+    owner[c] = (int32_t)blk;
+  }
+}
+
+// kernel table ---------------------------------------------------------------------------------
+constexpr int kCtaT = 256, kCtaE = 16;
+constexpr int kGrpE8 = 8, kGrpE32 = 16;
+
+template <int FORM>
+void *kernel_for(int lanes) {
+  switch (lanes) {
+    case 8: return (void *)k_epoch_group<FORM, 8, kGrpE8>;
+    case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
+    default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
+  }
+}
+
+EpochArgs make_args(scd_ctx *c) {
+  EpochArgs a;
+  a.ptr = c->ptr;
+  a.idx = c->idx;
+  a.val = c->val;
+  a.y = c->y;
+  a.norm = c->norm;
+  a.x = c->x;
+  a.sv = c->sv;
+  a.lam = c->lam;
+  a.lamN = c->lamN;
+  return a;
+}
+
+cudaEvent_t get_event(scd_ctx *c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+}  // namespace
+
+// Grid/block for a bin (used by build_schedule): persistent, sized to the SM count times the
+// kernel's residency, capped by max_inflight coordinates in flight.
+void bin_launch_shape(scd_ctx *c, Bin &b) {
+  void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
+  const int block = (b.lanes == 8 || b.lanes == 32) ? 256 : kCtaT;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, 0);
+  if (occ < 1) occ = 1;
+  int64_t grid = (int64_t)c->nsm * occ;
+  const int coords_per_cta = (b.lanes == 8 || b.lanes == 32) ? block / b.lanes : 1;
+  const int64_t cap = c->opt.max_inflight > 0 ? c->opt.max_inflight : c->auto_cap;  // staleness cap
+  if (cap > 0) {
+    int64_t g = (cap + coords_per_cta - 1) / coords_per_cta;
+    if (g < grid) grid = g;
+  }
+  int64_t need = (b.count + coords_per_cta - 1) / coords_per_cta;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  b.grid = (int)grid;
+  b.block = block;
+}
+
+scd_status run_epoch(scd_ctx *c, uint32_t epoch) {
+  EpochArgs a = make_args(c);
+  cudaStream_t s = c->stream;
+  if (c->opt.deterministic) {
+    Perm p = make_perm(c->opt.seed, epoch, 0u, c->n_coord);
+    if (c->form == SCD_PRIMAL)
+      k_epoch_debug<SCD_PRIMAL><<<1, kDbgT, 0, s>>>(a, p, c->n_coord);
+    else
+      k_epoch_debug<SCD_DUAL><<<1, kDbgT, 0, s>>>(a, p, c->n_coord);
+    SCD_CKL(c, "k_epoch_debug launch");
+    ++c->launches;
+    c->empty_dirty = false;
+    return SCD_OK;
+  }
+  if (c->empty_dirty && c->n_empty > 0) {
+    const int g = grid_for(c->n_empty, 256);
+    if (c->form == SCD_PRIMAL)
+      k_empty_fix<SCD_PRIMAL><<<g, 256, 0, s>>>(a, c->empty_list, c->n_empty);
+    else
+      k_empty_fix<SCD_DUAL><<<g, 256, 0, s>>>(a, c->empty_list, c->n_empty);
+    SCD_CKL(c, "k_empty_fix launch");
+    ++c->launches;
+  }
+  c->empty_dirty = false;
+  if (c->n_bins > 0) SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins, s));
+  for (int i = 0; i < c->n_bins; ++i) {
+    Bin &b = c->bins[i];
+    if (b.count == 0) continue;
+    BinArgs ba;
+    ba.list = b.list;
+    ba.count = b.count;
+    ba.counter = c->counters + i;
+    ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.count);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->opt.profile) {
+      e0 = get_event(c);
+      e1 = get_event(c);
+      cudaEventRecord(e0, s);
+    }
+    void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
+    void *args[] = {&a, &ba};
+    SCD_CK(c, cudaLaunchKernel(fn, dim3(b.grid), dim3(b.block), args, 0, s));
+    ++c->launches;
+    if (c->opt.profile) {
+      cudaEventRecord(e1, s);
+      c->ev_pending.push_back({i, {e0, e1}});
+    }
+  }
+  return SCD_OK;
+}
+
+scd_status profile_collect(scd_ctx *c) {
+  for (auto &p : c->ev_pending) {
+    float ms = 0.f;
+    SCD_CK(c, cudaEventSynchronize(p.second.second));
+    SCD_CK(c, cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+    c->bins[p.first].ms += ms;
+    c->bins[p.first].prof_launches += 1;
+    c->ev_pool.push_back(p.second.first);
+    c->ev_pool.push_back(p.second.second);
+  }
+  c->ev_pending.clear();
+  return SCD_OK;
+}
+
+scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out,
+                              cudaStream_t s) {
+  Perm p = make_perm(seed, epoch, stream, n);
+  k_perm_export<<<grid_for(n, 256), 256, 0, s>>>(p, n, d_out);
+  return cudaGetLastError() == cudaSuccess ? SCD_OK : SCD_E_CUDA;
+}
+
+scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s) {
+  Perm p = make_perm(seed, 0u, kPartStream, count);
+  k_partition_export<<<grid_for(count, 256), 256, 0, s>>>(p, count, k, d_owner);
+  return cudaGetLastError() == cudaSuccess ? SCD_OK : SCD_E_CUDA;
+}
+
+}  // namespace scd

@@ -1,0 +1,264 @@
+// layout.cu — create-time plumbing on the device: matrix validation, squared norms, the
+// asynchronous coordinate schedule (length bins), and the stable CSR<->CSC transpose.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace scd {
+namespace {
+
+// Matrix invariants (SPEC S:29-31 restated in scd.h): ptr[0] = 0, nondecreasing, ptr[outer] = nnz;
+// inner indices in range and strictly increasing per outer index.  *bad = first bad outer index.
+__global__ void k_validate(const int64_t *ptr, const int32_t *idx, int64_t outer, int64_t inner, int64_t nnz,
+                           unsigned long long *bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = warp; o < outer; o += nwarps) {
+    const int64_t beg = ptr[o], end = ptr[o + 1];
+    bool ok = beg <= end && beg >= 0 && end <= nnz;
+    if (o == 0 && beg != 0) ok = false;
+    if (o == outer - 1 && end != nnz) ok = false;
+    if (ok) {
+      for (int64_t k = beg + lane; k < end; k += 32) {
+        const int32_t i = idx[k];
+        if (i < 0 || i >= inner) ok = false;
+        if (k > beg && idx[k - 1] >= i) ok = false;
+      }
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok && lane == 0) atomicMin(bad, (unsigned long long)o);
+  }
+}
+
+// ||a||² of every outer index: fp64 accumulation in storage order per lane, rounded to fp32 (c9).
+__global__ void k_norms(const int64_t *ptr, const float *val, int64_t outer, float *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = warp; o < outer; o += nwarps) {
+    double s = 0.0;
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) {
+      const double v = val[k];
+      s += v * v;
+    }
+    s = warp_sum(s);
+    if (lane == 0) out[o] = (float)s;
+  }
+}
+
+// transpose helpers
+__global__ void k_outer_of(const int64_t *ptr, int64_t outer, int32_t *outer_of) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = warp; o < outer; o += nwarps)
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) outer_of[k] = (int32_t)o;
+}
+__global__ void k_iota64(int64_t *p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = i;
+}
+__global__ void k_count(const int32_t *keys, int64_t n, unsigned long long *cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + keys[i] + 1, 1ull);
+}
+__global__ void k_gather_t(const int64_t *perm, const int32_t *outer_of, const float *val, int64_t n, int32_t *oidx,
+                           float *oval) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = perm[i];
+    oidx[i] = outer_of[e];
+    oval[i] = val[e];
+  }
+}
+
+// s[idx[k]] += |val[k]|  (s = |A|ᵀ1 for CSR, |A|1 for CSC), fp64
+__global__ void k_abs_scatter(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, double *s) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = warp; o < outer; o += nwarps)
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) atomicAdd(s + idx[k], (double)fabsf(val[k]));
+}
+// acc[0] += Σ s_i², acc[1] += Σ norm_o
+__global__ void __launch_bounds__(256) k_coupling_sums(const double *s, int64_t n, const float *norm, int64_t nc,
+                                                       double *acc) {
+  double a = 0.0, b = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a += s[i] * s[i];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
+    b += (double)norm[i];
+  block_sum_atomic<256>(a, acc + 0);
+  block_sum_atomic<256>(b, acc + 1);
+}
+
+}  // namespace
+
+// Staleness bound for the asynchronous kernels.  With τ coordinates in flight a
+// coordinate's update sees up to τ concurrent updates it did not read.  Treating them as one
+// block-Jacobi step, the step stays contractive while τ·c̄ < λN + d̄ (diagonal dominance of the
+// coordinate Hessian block), where d̄ = mean ||a||² and c̄ = mean |<a_i, a_j>| over coordinate
+// pairs, estimated here from ||(|A|ᵀ1)||² = Σ_i Σ_j |<a_i,a_j>| (upper bound of the mean |.|).
+scd_status estimate_inflight_cap(scd_ctx *c) {
+  cudaStream_t s = c->stream;
+  double *vec = c->vec64;
+  SCD_CK(c, cudaMemsetAsync(vec, 0, sizeof(double) * (size_t)c->n_shared, s));
+  SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 2, s));
+  k_abs_scatter<<<grid_for(c->n_coord * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, c->n_coord, vec);
+  k_coupling_sums<<<grid_for(c->n_shared > c->n_coord ? c->n_shared : c->n_coord, 256, 148 * 8), 256, 0, s>>>(
+      vec, c->n_shared, c->norm, c->n_coord, c->acc);
+  SCD_CKL(c, "coupling estimate");
+  double h[2];
+  SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SCD_CK(c, cudaStreamSynchronize(s));
+  const double n = (double)(c->n_nonempty > 1 ? c->n_nonempty : 2);
+  const double cbar = (h[0] - h[1]) / (n * (n - 1.0));  // mean off-diagonal |<a_i, a_j>| (upper bound)
+  const double dbar = h[1] / n + c->lamN;
+  double tau = cbar > 0 ? dbar / cbar : 1e18;
+  c->tau_star = tau;
+  double cap = 0.5 * tau;
+  if (cap < 32) cap = 32;
+  if (cap > 1e9) cap = 1e9;
+  c->auto_cap = (int64_t)cap;
+  return SCD_OK;
+}
+
+scd_status validate_matrix(scd_ctx *c, int64_t outer, int64_t inner) {
+  unsigned long long *d_bad = nullptr;
+  SCD_CK(c, cudaMallocAsync((void **)&d_bad, sizeof(unsigned long long), c->stream));
+  SCD_CK(c, cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), c->stream));
+  k_validate<<<grid_for(outer * 32, 256), 256, 0, c->stream>>>(c->ptr, c->idx, outer, inner, c->nnz, d_bad);
+  SCD_CKL(c, "k_validate");
+  unsigned long long bad = 0;
+  SCD_CK(c, cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
+  SCD_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFreeAsync(d_bad, c->stream);
+  if (bad != ~0ull)
+    return fail(c, SCD_E_BAD_MATRIX, "matrix invariant violated at outer index " + std::to_string(bad));
+  return SCD_OK;
+}
+
+scd_status compute_norms(scd_ctx *c) {
+  k_norms<<<grid_for(c->n_coord * 32, 256), 256, 0, c->stream>>>(c->ptr, c->val, c->n_coord, c->norm);
+  SCD_CKL(c, "k_norms");
+  return SCD_OK;
+}
+
+// Asynchronous schedule: coordinates binned by stored-entry count, each bin processed by the
+// kernel shape that suits its length.  Empty coordinates go to the empty list.
+scd_status build_schedule(scd_ctx *c) {
+  const int64_t n = c->n_coord;
+  std::vector<int64_t> hp((size_t)n + 1);
+  SCD_CK(c, cudaMemcpyAsync(hp.data(), c->ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost, c->stream));
+  SCD_CK(c, cudaStreamSynchronize(c->stream));
+  // bin thresholds (entries per coordinate): (0,64] -> 8-lane groups, (64,1024] -> warps, >1024 -> CTA
+  const int64_t lim[3] = {64, 1024, INT64_MAX};
+  const int lanes[3] = {8, 32, 256};
+  std::vector<int32_t> lists[3], empty;
+  int64_t nnzb[3] = {0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t L = hp[(size_t)i + 1] - hp[(size_t)i];
+    if (L == 0) {
+      empty.push_back((int32_t)i);
+      continue;
+    }
+    for (int b = 0; b < 3; ++b)
+      if (L <= lim[b]) {
+        lists[b].push_back((int32_t)i);
+        nnzb[b] += L;
+        break;
+      }
+  }
+  c->n_empty = (int64_t)empty.size();
+  c->n_nonempty = n - c->n_empty;
+  if (c->n_empty) {
+    SCD_CK(c, cudaMalloc((void **)&c->empty_list, sizeof(int32_t) * empty.size()));
+    SCD_CK(c, cudaMemcpy(c->empty_list, empty.data(), sizeof(int32_t) * empty.size(), cudaMemcpyHostToDevice));
+  }
+  scd_status st = estimate_inflight_cap(c);
+  if (st != SCD_OK) return st;
+  // launch order: long coordinates first (CTA), then warps, then 8-lane groups
+  c->n_bins = 0;
+  const int order[3] = {2, 1, 0};
+  for (int oi = 0; oi < 3; ++oi) {
+    const int b = order[oi];
+    if (lists[b].empty()) continue;
+    Bin &B = c->bins[c->n_bins];
+    B.lanes = lanes[b];
+    B.count = (int64_t)lists[b].size();
+    B.nnz = nnzb[b];
+    B.stream_id = 1u + (uint32_t)c->n_bins;
+    if (B.count == n) {
+      B.list = nullptr;  // identity: every coordinate is in this bin
+    } else {
+      SCD_CK(c, cudaMalloc((void **)&B.list, sizeof(int32_t) * lists[b].size()));
+      SCD_CK(c, cudaMemcpy(B.list, lists[b].data(), sizeof(int32_t) * lists[b].size(), cudaMemcpyHostToDevice));
+    }
+    bin_launch_shape(c, B);
+    ++c->n_bins;
+  }
+  SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * kMaxBins));
+  return SCD_OK;
+}
+
+// Stable transpose on the device: stable radix sort of (inner index -> entry position), then
+// gather of the outer index and value.  Equal keys keep input order (increasing outer index).
+scd_status transpose_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
+                            int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, cudaStream_t s, std::string &err) {
+  auto ck = [&](cudaError_t e, const char *what) {
+    if (e != cudaSuccess) err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaSuccess;
+  };
+  int32_t *outer_of = nullptr, *keys_out = nullptr;
+  int64_t *pos_in = nullptr, *pos_out = nullptr;
+  unsigned long long *cnt = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  const int64_t n1 = nnz > 0 ? nnz : 1;
+  bool ok = ck(cudaMallocAsync((void **)&outer_of, sizeof(int32_t) * n1, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&keys_out, sizeof(int32_t) * n1, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&pos_in, sizeof(int64_t) * n1, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&pos_out, sizeof(int64_t) * n1, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&cnt, sizeof(unsigned long long) * (inner + 1), s), "alloc");
+  if (ok) {
+    cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (inner + 1), s);
+    if (nnz > 0) {
+      k_outer_of<<<grid_for(outer * 32, 256), 256, 0, s>>>(ptr, outer, outer_of);
+      k_iota64<<<grid_for(nnz, 256), 256, 0, s>>>(pos_in, nnz);
+      k_count<<<grid_for(nnz, 256), 256, 0, s>>>(idx, nnz, cnt);
+      int end_bit = 1;
+      while (end_bit < 32 && (1ll << end_bit) < inner) ++end_bit;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const uint32_t *)idx, (uint32_t *)keys_out, pos_in, pos_out,
+                                      nnz, 0, end_bit, s);
+      ok = ck(cudaMallocAsync(&tmp, tmp_bytes, s), "alloc sort tmp");
+      if (ok) {
+        ok = ck(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, (const uint32_t *)idx, (uint32_t *)keys_out, pos_in,
+                                                pos_out, nnz, 0, end_bit, s),
+                "radix sort");
+      }
+      if (ok) k_gather_t<<<grid_for(nnz, 256), 256, 0, s>>>(pos_out, outer_of, val, nnz, oidx, oval);
+    }
+    if (ok) {
+      // counts (cnt[0] = 0) -> inclusive scan = offsets
+      size_t sb = 0;
+      cub::DeviceScan::InclusiveSum(nullptr, sb, cnt, (unsigned long long *)optr, inner + 1, s);
+      void *tmp2 = nullptr;
+      ok = ck(cudaMallocAsync(&tmp2, sb, s), "alloc scan tmp") &&
+           ck(cub::DeviceScan::InclusiveSum(tmp2, sb, cnt, (unsigned long long *)optr, inner + 1, s), "scan");
+      if (tmp2) cudaFreeAsync(tmp2, s);
+    }
+    ok = ok && ck(cudaGetLastError(), "transpose kernels");
+  }
+  if (tmp) cudaFreeAsync(tmp, s);
+  if (outer_of) cudaFreeAsync(outer_of, s);
+  if (keys_out) cudaFreeAsync(keys_out, s);
+  if (pos_in) cudaFreeAsync(pos_in, s);
+  if (pos_out) cudaFreeAsync(pos_out, s);
+  if (cnt) cudaFreeAsync(cnt, s);
+  return ok ? SCD_OK : SCD_E_CUDA;
+}
+
+}  // namespace scd

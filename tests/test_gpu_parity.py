@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element on the
+same seeded inputs.  Tolerances:
+  integer artefacts (permutation, partition, transpose, generator twin): bit-exact
+  deterministic-mode model per epoch: ||x_gpu - x_orc||_inf / ||x_orc||_inf <= 1e-4  (BASELINE north_star)
+  objective / gap kernels on the same fp32 model: relative 1e-9 (fp64 vs fp64, reduction order only)
+  asynchronous solver: objective within 1e-5 relative of the oracle optimum and gap <= 1e-5
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import ridge, solver
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1702_07005_b200 as scd  # noqa: E402
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _rel(a, b):
+    return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def c2s():
+    """C2 (BASELINE configs[1]) sample: first 4000 rows, all 50k columns (many empty)."""
+    d = synth.gen_host(synth.CONFIGS["C2"].with_rows(4000))
+    return d, solver.Problem.from_csr(d)
+
+
+# ------------------------------------------------------------------ integer artefacts
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 1000, 4096, 4097, 350_000])
+def test_permutation_bit_exact(n):
+    for t, st in ((0, 0), (1, 0), (5, 3), (123456, 1)):
+        assert np.array_equal(scd.permutation(77, t, n, st), oracle.permutation(77, t, n, st))
+
+
+@pytest.mark.parametrize("count,k", [(0, 3), (5, 2), (8, 8), (1000, 7), (680_715, 8)])
+def test_partition_bit_exact(count, k):
+    assert np.array_equal(scd.partition(4, count, k), oracle.partition(4, count, k))
+
+
+@pytest.mark.parametrize("empty", [(0, 0), (3, 2)])
+def test_transpose_bit_exact(empty):
+    d = synth.random_sparse(301, 97, 0.07, 8, empty_rows=empty[0], empty_cols=empty[1])
+    ref = oracle.transpose(d["ptr"], d["idx"], d["val"], 97)
+    got = scd.transpose(d["ptr"], d["idx"], d["val"], 301, 97, "csr")
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+    gd = scd.transpose(_dev(d["ptr"]), _dev(d["idx"]), _dev(d["val"]), 301, 97, "csr")
+    for a, b in zip(gd, ref):
+        assert np.array_equal(a.cpu().numpy(), b)
+    back = scd.transpose(*ref, 301, 97, "csc")
+    for a, b in zip(back, (d["ptr"], d["idx"], d["val"])):
+        assert np.array_equal(a, b)
+
+
+def test_transpose_c2_sample_bit_exact(c2s):
+    d, pr = c2s
+    got = scd.transpose(d["ptr"], d["idx"], d["val"], pr.N, pr.M, "csr")
+    assert all(np.array_equal(a, b) for a, b in zip(got, (pr.cptr, pr.cidx, pr.cval)))
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C2"].with_rows(3000), synth.CONFIGS["C3"].with_rows(300),
+                                 synth.c5_scaled(20_000, 1e-3)], ids=["C2", "C3", "C5s"])
+def test_generator_device_twin_bit_exact(cfg):
+    h = synth.gen_host(cfg)
+    g = synth.gen_device(cfg)
+    for k in ("ptr", "idx", "val", "y"):
+        assert np.array_equal(g[k].cpu().numpy(), h[k]), k
+    # a window that starts mid-matrix
+    g2 = synth.gen_device(cfg, row0=101, nrows=57)
+    h2 = synth.gen_host(cfg, row0=101, nrows=57)
+    for k in ("ptr", "idx", "val", "y"):
+        assert np.array_equal(g2[k].cpu().numpy(), h2[k]), k
+
+
+# ------------------------------------------------------------------ deterministic epochs vs Alg. 1
+def _debug_parity(d, pr, form, epochs, seed, tol=1e-4):
+    if form == "dual":
+        s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=seed, deterministic=True)
+        x, sv = np.zeros(pr.N), np.zeros(pr.M)
+    else:
+        s = scd.Solver(pr.cptr, pr.cidx, pr.cval, pr.N, pr.M, d["y"], pr.lam, "primal", seed=seed,
+                       deterministic=True)
+        x, sv = np.zeros(pr.M), np.zeros(pr.N)
+    errs = []
+    for t in range(1, epochs + 1):
+        s.epoch(t)
+        if form == "dual":
+            solver.dual_epoch(pr, x, sv, oracle.permutation(seed, t, pr.N))
+        else:
+            solver.primal_epoch(pr, x, sv, oracle.permutation(seed, t, pr.M))
+        errs.append(_rel(s.get_model(), x))
+        assert errs[-1] <= tol, (form, t, errs)
+    assert _rel(s.get_shared(), sv) <= 10 * tol
+    # bitwise repeatable
+    s2 = scd.Solver(*((d["ptr"], d["idx"], d["val"]) if form == "dual" else (pr.cptr, pr.cidx, pr.cval)), pr.N, pr.M,
+                    d["y"], pr.lam, form, seed=seed, deterministic=True)
+    for t in range(1, epochs + 1):
+        s2.epoch(t)
+    assert np.array_equal(s2.get_model(), s.get_model())
+    return s, x, errs
+
+
+@pytest.mark.parametrize("form", ["dual", "primal"])
+def test_debug_epochs_match_oracle_c2(c2s, form):
+    d, pr = c2s
+    _debug_parity(d, pr, form, 4, seed=5)
+
+
+def test_debug_primal_c1_dense_and_closed_form():
+    d = synth.gen_host(synth.CONFIGS["C1"])
+    pr = solver.Problem.from_csr(d)
+    s, x, _ = _debug_parity(d, pr, "primal", 6, seed=1)
+    for t in range(7, 40):
+        s.epoch(t)
+    bstar = ridge.closed_form(pr.A(), pr.y, pr.lam)
+    assert _rel(s.get_model(), bstar) <= 1e-4
+
+
+@pytest.mark.parametrize("form", ["dual", "primal"])
+def test_debug_edge_cases_empty_and_ragged(form):
+    d = synth.random_sparse(257, 129, 0.05, 21, empty_rows=5, empty_cols=7)
+    d["lam"] = 0.01
+    pr = solver.Problem.from_csr(d)
+    _debug_parity(d, pr, form, 3, seed=9)
+
+
+def test_single_coordinate_and_single_row():
+    d = dict(ptr=np.array([0, 3], np.int64), idx=np.array([0, 2, 5], np.int32),
+             val=np.array([0.5, -1.0, 2.0], np.float32), y=np.array([1.0], np.float32), n_rows=1, n_cols=6, lam=0.1)
+    pr = solver.Problem.from_csr(d)
+    _debug_parity(d, pr, "dual", 2, seed=1)
+    _debug_parity(d, pr, "primal", 2, seed=1)
+
+
+# ------------------------------------------------------------------ objective / gap kernels
+@pytest.mark.parametrize("form", ["dual", "primal"])
+def test_objective_and_gap_kernels_match_oracle(c2s, form):
+    d, pr = c2s
+    A = pr.A()
+    args = (d["ptr"], d["idx"], d["val"]) if form == "dual" else (pr.cptr, pr.cidx, pr.cval)
+    s = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=2)
+    for t in range(1, 3):
+        s.epoch(t)
+    x = s.get_model().astype(np.float64)
+    P, D = s.objective()
+    g = s.duality_gap()
+    if form == "dual":
+        Po = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+        Do = ridge.dual_objective(A, pr.y, pr.lam, x)
+        go = ridge.gap_dual_gradform(A, pr.y, pr.lam, x)
+        gp = ridge.gap_dual(A, pr.y, pr.lam, x)
+    else:
+        Po = ridge.primal_objective(A, pr.y, pr.lam, x)
+        Do = ridge.dual_objective(A, pr.y, pr.lam, ridge.primal_to_dual(A, pr.y, x))
+        go = ridge.gap_primal_gradform(A, pr.y, pr.lam, x)
+        gp = ridge.gap_primal(A, pr.y, pr.lam, x)
+    assert P == pytest.approx(Po, rel=1e-9)
+    assert D == pytest.approx(Do, rel=1e-9)
+    assert g == pytest.approx(go, rel=1e-7, abs=1e-15)
+    assert abs(P - D) == pytest.approx(gp, rel=1e-3, abs=1e-9)
+
+
+def test_set_model_rebuilds_shared_vector(c2s):
+    d, pr = c2s
+    A = pr.A()
+    s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=2)
+    rng = np.random.default_rng(0)
+    a = (rng.standard_normal(pr.N) * 1e-3).astype(np.float32)
+    s.set_model(a)
+    np.testing.assert_allclose(s.get_shared(), A.T @ a.astype(np.float64), rtol=1e-5, atol=1e-7)
+    assert np.array_equal(s.get_model(), a)
+
+
+# ------------------------------------------------------------------ asynchronous epochs
+@pytest.fixture(scope="module")
+def c2full():
+    """Config C2 (BASELINE configs[1]) at full size: 100k x 50k, 5e7 nnz."""
+    d = synth.gen_host(synth.CONFIGS["C2"])
+    return d, solver.Problem.from_csr(d)
+
+
+@pytest.mark.parametrize("form", ["dual", "primal"])
+def test_async_converges_to_oracle_optimum(c2full, form):
+    """TPA-SCD asynchronous epochs reach the oracle's optimum: objective within 1e-5 relative,
+    gap <= 1e-5 (BASELINE north_star); per-epoch gap within a band of the sequential one
+    ("near-perfect convergence ... as a function of epochs")."""
+    d, pr = c2full
+    A = pr.A()
+    E = 20
+    xs, _, hist = solver.solve(pr, form, E, seed=4)
+    args = (d["ptr"], d["idx"], d["val"]) if form == "dual" else (pr.cptr, pr.cidx, pr.cval)
+    s = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=4)
+    print("schedule", s.info())
+    gaps = []
+    for t in range(1, E + 1):
+        s.epoch(t)
+        gaps.append(s.duality_gap())
+    x = s.get_model().astype(np.float64)
+    if form == "dual":
+        Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+    else:
+        Pg = ridge.primal_objective(A, pr.y, pr.lam, x)
+    Pstar = hist[-1]["P"]
+    print(form, "gpu gaps", ["%.2e" % g for g in gaps])
+    print(form, "seq gaps", ["%.2e" % h["gap"] for h in hist])
+    assert abs(Pg - Pstar) <= 1e-5 * abs(Pstar)
+    assert gaps[-1] <= 1e-5
+    for t in (0, 2, 5):  # early epochs: same order of magnitude as the sequential trajectory
+        assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
+
+
+def test_async_short_rows_group_kernel():
+    """Criteo-shaped rows (39 one-hot fields) run on the 8-lane group kernel."""
+    cfg = synth.c5_scaled(30_000, 1e-3)
+    d = synth.gen_host(cfg)
+    pr = solver.Problem.from_csr(d)
+    s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=1)
+    assert s.info()["bins"][0]["lanes"] == 8
+    xs, _, hist = solver.solve(pr, "dual", 15, seed=1)
+    for t in range(1, 16):
+        s.epoch(t)
+    g = s.duality_gap()
+    assert g <= max(10 * hist[-1]["gap"], 1e-7), (g, hist[-1]["gap"])
+
+
+# ------------------------------------------------------------------ aggregation (Alg. 3 / 4)
+def _shards(d, pr, form, K, seed_part):
+    n = pr.M if form == "primal" else pr.N
+    owner = oracle.partition(seed_part, n, K)
+    out = []
+    for k in range(K):
+        loc = np.nonzero(owner == k)[0]
+        if form == "primal":
+            p = np.concatenate([[0], np.cumsum(np.diff(pr.cptr)[loc])]).astype(np.int64)
+            sel = np.concatenate([np.arange(pr.cptr[c], pr.cptr[c + 1]) for c in loc]) if len(loc) else np.zeros(0, int)
+            out.append((p, pr.cidx[sel], pr.cval[sel], pr.N, len(loc), d["y"]))
+        else:
+            p = np.concatenate([[0], np.cumsum(np.diff(pr.rptr)[loc])]).astype(np.int64)
+            sel = np.concatenate([np.arange(pr.rptr[r], pr.rptr[r + 1]) for r in loc])
+            out.append((p, pr.ridx[sel], pr.rval[sel], len(loc), pr.M, d["y"][loc]))
+    return out
+
+
+@pytest.mark.parametrize("form", ["primal", "dual"])
+@pytest.mark.parametrize("mode", ["average", "optimal", "add"])
+def test_logical_k_aggregation_matches_oracle(form, mode):
+    d = synth.gen_host(synth.CONFIGS["C2"].with_rows(1500))
+    pr = solver.Problem.from_csr(d)
+    K, seed, sp_ = 4, 10, 3
+    rounds = 4 if mode != "add" else 2
+    xo, so, hist = solver.run_distributed(pr, form, K, mode, rounds, seed=seed, seed_part=sp_)
+    solvers = [scd.Solver(p, i, v, nr, nc, y, pr.lam, form, seed=seed + k, deterministic=True, n_global=pr.N)
+               for k, (p, i, v, nr, nc, y) in enumerate(_shards(d, pr, form, K, sp_))]
+    for t in range(1, rounds + 1):
+        for s in solvers:
+            s.epoch(t)
+        g = scd.aggregate_group(solvers, mode)
+        assert g == pytest.approx(hist[t - 1]["gamma"], rel=1e-4, abs=1e-7), (t, g, hist[t - 1]["gamma"])
+    owner = oracle.partition(sp_, pr.M if form == "primal" else pr.N, K)
+    x = np.zeros(len(owner))
+    for k, s in enumerate(solvers):
+        x[owner == k] = s.get_model()
+    assert _rel(x, xo) <= 1e-4
+    assert _rel(solvers[0].get_shared(), so) <= 1e-4
+
+
+@pytest.mark.parametrize("form", ["primal", "dual"])
+def test_nccl_single_rank_aggregate_and_gap(c2s, form):
+    """The NCCL code path (all-reduce of Δ and the scalars, all-reduce inside the gap) with a
+    1-rank communicator must equal the communicator-free result."""
+    d, pr = c2s
+    uid = scd.nccl_unique_id()
+    comm = scd.nccl_comm_init(uid, 1, 0)
+    args = (d["ptr"], d["idx"], d["val"]) if form == "dual" else (pr.cptr, pr.cidx, pr.cval)
+    a = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=3, deterministic=True, nccl_comm=comm)
+    b = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=3, deterministic=True)
+    for t in (1, 2):
+        a.epoch(t)
+        b.epoch(t)
+        assert a.aggregate("optimal") == pytest.approx(b.aggregate("optimal"), rel=1e-12)
+    assert np.array_equal(a.get_model(), b.get_model())
+    assert a.duality_gap() == pytest.approx(b.duality_gap(), rel=1e-9)
+    a.close()
+    scd.nccl_comm_destroy(comm)
+
+
+# ------------------------------------------------------------------ errors
+def test_bad_matrix_rejected():
+    from paper_1702_07005_b200.scd import ScdError
+
+    ptr = np.array([0, 2, 3], np.int64)
+    idx = np.array([3, 1, 0], np.int32)  # row 0 not strictly increasing
+    with pytest.raises(ScdError) as e:
+        scd.Solver(ptr, idx, np.ones(3, np.float32), 2, 4, np.ones(2, np.float32), 1.0, "dual")
+    assert e.value.status == 2 and "outer index 0" in str(e.value)
+    idx = np.array([1, 3, 9], np.int32)  # out of range in row 1
+    with pytest.raises(ScdError) as e:
+        scd.Solver(ptr, idx, np.ones(3, np.float32), 2, 4, np.ones(2, np.float32), 1.0, "dual")
+    assert e.value.status == 2 and "outer index 1" in str(e.value)
+
+
+def test_empty_matrix_dual_fixed_point():
+    """nnz = 0: every row is empty; one epoch lands on α_n = y_n/N (c17), gap 0."""
+    n = 10
+    y = np.linspace(-1, 1, n).astype(np.float32)
+    s = scd.Solver(np.zeros(n + 1, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32), n, 3, y, 0.5, "dual")
+    s.epoch(1)
+    np.testing.assert_allclose(s.get_model(), y / n, rtol=1e-6)
+    assert s.duality_gap() <= 1e-12
