@@ -161,7 +161,10 @@ typedef struct {
   int64_t launches;       /* kernels launched by the context since create (cumulative) */
   double tau_star;        /* estimated staleness bound: coordinates in flight before the asynchronous
                              step stops being contractive */
-  int64_t inflight_cap;   /* coordinates in flight actually allowed (max_inflight or tau_star/2) */
+  int64_t inflight_cap;   /* largest per-bin cap on coordinates in flight */
+  int64_t bin_cap[4];     /* per bin: coordinates in flight allowed (max_inflight, else bin_tau/2) */
+  double bin_tau[4];      /* per bin: estimated staleness bound */
+  int32_t n_slices;       /* the bins are interleaved in this many slices per epoch (reading c24) */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

@@ -330,7 +330,13 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   }
   info->launches = c->launches;
   info->tau_star = c->tau_star;
-  info->inflight_cap = c->opt.max_inflight > 0 ? c->opt.max_inflight : c->auto_cap;
+  info->n_slices = c->n_slices;
+  info->inflight_cap = 0;
+  for (int i = 0; i < c->n_bins && i < 4; ++i) {
+    info->bin_cap[i] = c->bins[i].cap;
+    info->bin_tau[i] = c->bins[i].tau;
+    if (c->bins[i].cap > info->inflight_cap) info->inflight_cap = c->bins[i].cap;
+  }
   return SCD_OK;
 }
 

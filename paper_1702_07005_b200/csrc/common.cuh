@@ -13,6 +13,7 @@
 namespace scd {
 
 constexpr int kMaxBins = 4;
+constexpr int kMaxSlices = 64;
 constexpr uint32_t kPartStream = 0x50415254u;  // "PART": partition permutation stream (c15)
 
 // ------------------------------------------------------------------------------------------
@@ -70,8 +71,15 @@ __device__ __forceinline__ uint64_t perm_apply(const Perm &p, uint64_t j) {
 // ------------------------------------------------------------------------------------------
 // Context
 // ------------------------------------------------------------------------------------------
+constexpr int kLanesCta = 256;       // bin kind: one CTA of 256 threads per coordinate
+constexpr int kClusterCtas = 8;      // portable cluster size
+constexpr int kClusterThreads = 512;
+constexpr int kLanesCluster = kClusterCtas * kClusterThreads;  // bin kind: one 8-CTA cluster per coordinate
+
 struct Bin {
-  int lanes = 0;             // lanes per coordinate: 8 / 32 (sub-warp group) or blockDim (CTA)
+  int lanes = 0;             // lanes per coordinate: 8 / 32 (sub-warp group), 256 (CTA), 4096 (cluster)
+  double tau = 0.0;          // estimated staleness bound of the bin (coordinates in flight)
+  int64_t cap = 0;           // coordinates in flight allowed
   int64_t count = 0, nnz = 0;
   int32_t *list = nullptr;   // device, coordinate ids ascending
   int grid = 0, block = 0;
@@ -109,7 +117,8 @@ struct scd_ctx {
   int32_t *empty_list = nullptr;
   int64_t n_empty = 0, n_nonempty = 0;
   bool empty_dirty = true;
-  unsigned int *counters = nullptr;  // [kMaxBins] ticket counters
+  int n_slices = 1;                  // bins are interleaved in n_slices slices per epoch
+  unsigned int *counters = nullptr;  // [kMaxSlices * kMaxBins] ticket counters
   // scratch
   double *acc = nullptr;    // [32] fp64 accumulators (objective / gap / gamma)
   double *vec64 = nullptr;  // [n_shared] fp64 (u = Aβ or v = Aᵀα)
@@ -120,8 +129,7 @@ struct scd_ctx {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
   int64_t launches = 0;
   uint32_t epochs_done = 0;
-  double tau_star = 0.0;   // estimated staleness bound (coordinates in flight), layout.cu
-  int64_t auto_cap = 0;    // default max coordinates in flight = tau_star / 2
+  double tau_star = 0.0;   // smallest estimated staleness bound over the bins (layout.cu)
   std::string err;
 };
 
@@ -154,7 +162,7 @@ void set_global_error(const std::string &msg);
 scd_status validate_matrix(scd_ctx *c, int64_t outer, int64_t inner);
 scd_status compute_norms(scd_ctx *c);
 scd_status build_schedule(scd_ctx *c);
-scd_status estimate_inflight_cap(scd_ctx *c);
+scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau);
 scd_status transpose_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
                             int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, cudaStream_t s, std::string &err);
 

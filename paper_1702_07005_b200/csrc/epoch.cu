@@ -19,6 +19,8 @@
 //                            order, fixed reduction tree -> bitwise repeatable (oracle parity).
 //   k_empty_fix<FORM>        coordinates with no stored entry: Δ = -β_m (primal) / y_n/N - α_n (dual)
 //                            (c17); only re-run when the model was set externally.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace scd {
@@ -37,7 +39,7 @@ struct EpochArgs {
 
 struct BinArgs {
   const int32_t *list;  // coordinate ids of the bin (ascending); nullptr = identity
-  int64_t count;
+  int64_t lo, hi;       // this launch processes permutation positions [lo, hi) of the bin
   unsigned int *counter;
   Perm perm;
 };
@@ -64,6 +66,102 @@ __device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
 }
 
 // ----------------------------------------------------------------------------------------------
+// Two-pass streaming CTA kernel (one coordinate per CTA).  Pass 1 streams the coordinate's
+// (idx, val) from HBM with coalesced loads, U independent gathers in flight per thread; pass 2
+// re-reads (idx, val) — now L2-resident — for the atomic scatter.  Holding nothing in registers
+// between the passes keeps the kernel at ~32 registers, i.e. full occupancy (64 warps/SM), which
+// is what hides the idx -> gather -> reduce -> scatter latency chain (the register-resident
+// variant below ran at 50% occupancy and was latency-bound).  Thread 0 software-pipelines the
+// schedule: the next ticket's atomic is issued before pass 1 and its coordinate / offsets are
+// fetched before pass 2, so neither latency sits on the critical path.
+template <int FORM, int T, int U>
+__global__ void __launch_bounds__(T, 2048 / T) k_epoch_stream(EpochArgs a, BinArgs b) {
+  constexpr int NW = T / 32;
+  __shared__ float s_red[NW];
+  __shared__ float s_delta;
+  __shared__ long long s_c, s_beg, s_end;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // thread 0: schedule state for the next coordinate
+  long long nc = -1, nbeg = 0, nend = 0;
+  if (tid == 0) {
+    const int64_t t = b.lo + (int64_t)atomicAdd(b.counter, 1u);
+    if (t < b.hi) {
+      nc = bin_coord(b, (uint64_t)t);
+      nbeg = __ldg(a.ptr + nc);
+      nend = __ldg(a.ptr + nc + 1);
+    }
+  }
+  for (;;) {
+    unsigned int nticket = 0;
+    if (tid == 0) {
+      s_c = nc;
+      s_beg = nbeg;
+      s_end = nend;
+      if (nc >= 0) nticket = atomicAdd(b.counter, 1u);  // next ticket, consumed after pass 1
+    }
+    __syncthreads();
+    const long long c = s_c;
+    if (c < 0) break;
+    const int64_t beg = s_beg, end = s_end;
+    float xc = 0.f, nrm = 0.f, yc = 0.f;
+    if (tid == 0) {  // consumed after the reduction
+      xc = a.x[c];
+      nrm = __ldg(a.norm + c);
+      if (FORM == SCD_DUAL) yc = __ldg(a.y + c);
+    }
+    // pass 1: gather-dot
+    float acc = 0.f;
+    for (int64_t base = beg + tid; base < end; base += (int64_t)T * U) {
+      int32_t id[U];
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = base + (int64_t)u * T;
+        id[u] = k < end ? __ldcg(a.idx + k) : -1;
+        v[u] = k < end ? __ldcg(a.val + k) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (id[u] >= 0) acc = fmaf(ld_sv(a.sv + id[u]), v[u], acc);
+    }
+    if (tid == 0) {  // schedule the next coordinate while the block reduces / scatters
+      const int64_t t = b.lo + (int64_t)nticket;
+      nc = -1;
+      if (t < b.hi) {
+        nc = bin_coord(b, (uint64_t)t);
+        nbeg = __ldg(a.ptr + nc);
+        nend = __ldg(a.ptr + nc + 1);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+      float s = lane < NW ? s_red[lane] : 0.f;
+      s = warp_sum(s);
+      if (lane == 0) {
+        const float d = coord_delta<FORM>(s, xc, nrm, yc, a.lam, a.lamN);
+        a.x[c] = xc + d;  // single writer per epoch (c10)
+        s_delta = d;
+      }
+    }
+    __syncthreads();
+    const float d = scatter_scale<FORM>(s_delta);
+    if (d != 0.f) {
+      for (int64_t base = beg + tid; base < end; base += (int64_t)T * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t k = base + (int64_t)u * T;
+          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Register-resident CTA kernel (first version, kept for comparison): E entries per thread held
+// in registers between the gather-dot and the scatter.
 template <int FORM, int T, int E>
 __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
   constexpr int NW = T / 32;
@@ -74,8 +172,8 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
   for (;;) {
     if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
     __syncthreads();
-    const unsigned int t = s_ticket;
-    if (t >= (uint64_t)b.count) break;
+    const int64_t t = b.lo + (int64_t)s_ticket;
+    if (t >= b.hi) break;
     const int64_t c = bin_coord(b, t);
     const int64_t beg = __ldg(a.ptr + c), end = __ldg(a.ptr + c + 1);
     int32_t id[E];
@@ -145,10 +243,10 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
     unsigned int t0 = 0;
     if (lane == 0) t0 = atomicAdd(b.counter, (unsigned)CPW);
     t0 = __shfl_sync(0xffffffffu, t0, 0);
-    if (t0 >= (uint64_t)b.count) break;  // warp-uniform
+    if (b.lo + (int64_t)t0 >= b.hi) break;  // warp-uniform
     // lanes 0..CPW-1 evaluate the permutation for the warp's CPW tickets, then broadcast
     int64_t cl = -1;
-    if (lane < CPW && t0 + lane < (uint64_t)b.count) cl = bin_coord(b, t0 + lane);
+    if (lane < CPW && b.lo + (int64_t)t0 + lane < b.hi) cl = bin_coord(b, b.lo + t0 + lane);
     const int64_t c = __shfl_sync(0xffffffffu, cl, sub);
     const bool active = c >= 0;
     int64_t beg = 0, end = 0;
@@ -261,16 +359,113 @@ __global__ void k_partition_export(Perm p, int64_t count, int32_t k, int32_t *ow
   }
 }
 
+// ----------------------------------------------------------------------------------------------
+// Very long coordinates (> 16384 entries: the dense head of a power-law feature distribution in
+// the primal) are strongly coupled to one another, so only a few may be in flight.
+// To keep the GPU busy anyway, each one is split across a cluster of CL CTAs: every CTA takes a
+// contiguous slice, partial dots meet in CTA 0's shared memory over DSMEM, CTA 0 computes Δ, and
+// every CTA scatters its slice.  Two cluster barriers per coordinate.
+template <int FORM, int CL, int T, int E>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(EpochArgs a, BinArgs b) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int NW = T / 32;
+  __shared__ float s_red[NW];
+  __shared__ float s_part[CL];
+  __shared__ float s_delta;
+  __shared__ unsigned int s_ticket;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned int r = cluster.block_rank();
+  unsigned int *ticket0 = cluster.map_shared_rank(&s_ticket, 0);
+  float *part0 = cluster.map_shared_rank(s_part, 0);
+  float *delta0 = cluster.map_shared_rank(&s_delta, 0);
+  for (;;) {
+    if (r == 0 && tid == 0) s_ticket = atomicAdd(b.counter, 1u);
+    cluster.sync();
+    const int64_t t = b.lo + (int64_t)*ticket0;
+    if (t >= b.hi) {
+      cluster.sync();  // nobody leaves while another CTA may still read CTA 0's shared memory
+      break;
+    }
+    const int64_t c = bin_coord(b, t);
+    const int64_t beg0 = __ldg(a.ptr + c), end0 = __ldg(a.ptr + c + 1);
+    const int64_t slice = (end0 - beg0 + CL - 1) / CL;
+    const int64_t beg = beg0 + (int64_t)r * slice;
+    const int64_t end = min(end0, beg + slice);
+    int32_t id[E];
+    float v[E];
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = beg + (int64_t)e * T + tid;
+      if (k < end) {
+        id[e] = __ldcs(a.idx + k);
+        v[e] = __ldcs(a.val + k);
+      } else {
+        id[e] = -1;
+        v[e] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
+    for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
+#pragma unroll 4
+      for (int e = 0; e < E; ++e) {
+        const int64_t k = base + (int64_t)e * T + tid;
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+      float s = lane < NW ? s_red[lane] : 0.f;
+      s = warp_sum(s);
+      if (lane == 0) part0[r] = s;
+    }
+    cluster.sync();
+    if (r == 0 && tid == 0) {
+      float s = 0.f;
+      for (int i = 0; i < CL; ++i) s += s_part[i];
+      const float xc = a.x[c];
+      const float d = coord_delta<FORM>(s, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f, a.lam,
+                                        a.lamN);
+      a.x[c] = xc + d;
+      s_delta = d;
+    }
+    cluster.sync();
+    const float d = scatter_scale<FORM>(*delta0);
+    if (d != 0.f) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
+      for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
+#pragma unroll 4
+        for (int e = 0; e < E; ++e) {
+          const int64_t k = base + (int64_t)e * T + tid;
+          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
+        }
+      }
+    }
+  }
+}
+
 // kernel table ---------------------------------------------------------------------------------
-constexpr int kCtaT = 256, kCtaE = 16;
+constexpr int kCtaT = kLanesCta, kCtaE = 16, kStreamU = 4;
 constexpr int kGrpE8 = 8, kGrpE32 = 16;
+constexpr int kClE = 8;
 
 template <int FORM>
 void *kernel_for(int lanes) {
   switch (lanes) {
     case 8: return (void *)k_epoch_group<FORM, 8, kGrpE8>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
-    default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
+    case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE>;
+    default: {
+      static const bool regs = getenv("SCD_CTA_KERNEL") && std::string(getenv("SCD_CTA_KERNEL")) == "regs";
+      return regs ? (void *)k_epoch_cta<FORM, kCtaT, kCtaE> : (void *)k_epoch_stream<FORM, kCtaT, kStreamU>;
+    }
   }
 }
 
@@ -305,21 +500,30 @@ cudaEvent_t get_event(scd_ctx *c) {
 // kernel's residency, capped by max_inflight coordinates in flight.
 void bin_launch_shape(scd_ctx *c, Bin &b) {
   void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
-  const int block = (b.lanes == 8 || b.lanes == 32) ? 256 : kCtaT;
+  const bool group = (b.lanes == 8 || b.lanes == 32);
+  const bool clus = (b.lanes == kLanesCluster);
+  int block = group ? 256 : (clus ? kClusterThreads : kCtaT);
+  // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
+  if (group && b.cap > 0 && b.cap * b.lanes < block) {
+    block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
+    if (block < 32) block = 32;
+  }
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, 0);
   if (occ < 1) occ = 1;
-  int64_t grid = (int64_t)c->nsm * occ;
-  const int coords_per_cta = (b.lanes == 8 || b.lanes == 32) ? block / b.lanes : 1;
-  const int64_t cap = c->opt.max_inflight > 0 ? c->opt.max_inflight : c->auto_cap;  // staleness cap
-  if (cap > 0) {
-    int64_t g = (cap + coords_per_cta - 1) / coords_per_cta;
-    if (g < grid) grid = g;
+  const int per_launch_unit = clus ? kClusterCtas : 1;           // CTAs per coordinate slot
+  const int coords_per_cta = group ? block / b.lanes : 1;
+  int64_t slots = (int64_t)c->nsm * occ / per_launch_unit;        // resident coordinate slots
+  if (clus && slots > (int64_t)c->nsm / kClusterCtas * occ) slots = (int64_t)c->nsm / kClusterCtas * occ;
+  int64_t units = group ? slots : slots;                          // CTAs (or clusters)
+  if (b.cap > 0) {  // staleness cap
+    int64_t u = (b.cap + coords_per_cta - 1) / coords_per_cta;
+    if (u < units) units = u;
   }
   int64_t need = (b.count + coords_per_cta - 1) / coords_per_cta;
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
-  b.grid = (int)grid;
+  if (units > need) units = need;
+  if (units < 1) units = 1;
+  b.grid = (int)(units * per_launch_unit);
   b.block = block;
 }
 
@@ -347,28 +551,42 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch) {
     ++c->launches;
   }
   c->empty_dirty = false;
-  if (c->n_bins > 0) SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins, s));
-  for (int i = 0; i < c->n_bins; ++i) {
-    Bin &b = c->bins[i];
-    if (b.count == 0) continue;
-    BinArgs ba;
-    ba.list = b.list;
-    ba.count = b.count;
-    ba.counter = c->counters + i;
-    ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.count);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (c->opt.profile) {
-      e0 = get_event(c);
-      e1 = get_event(c);
-      cudaEventRecord(e0, s);
-    }
-    void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
-    void *args[] = {&a, &ba};
-    SCD_CK(c, cudaLaunchKernel(fn, dim3(b.grid), dim3(b.block), args, 0, s));
-    ++c->launches;
-    if (c->opt.profile) {
-      cudaEventRecord(e1, s);
-      c->ev_pending.push_back({i, {e0, e1}});
+  if (c->n_bins == 0) return SCD_OK;
+  // The epoch visits each bin in its own random order; the bins are interleaved in S slices so
+  // that, at the granularity of a slice, the epoch order stays a random mix of all coordinates
+  // (a bin-by-bin order converges much more slowly, DESIGN.md §6 / reading c24).
+  const int S = c->n_slices;
+  SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins * S, s));
+  for (int sl = 0; sl < S; ++sl) {
+    for (int i = 0; i < c->n_bins; ++i) {
+      Bin &b = c->bins[i];
+      BinArgs ba;
+      ba.list = b.list;
+      ba.lo = b.count * sl / S;
+      ba.hi = b.count * (sl + 1) / S;
+      if (ba.hi <= ba.lo) continue;
+      ba.counter = c->counters + sl * kMaxBins + i;
+      ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.count);
+      const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;  // coordinates per CTA (or cluster)
+      const int unit = b.lanes == kLanesCluster ? kClusterCtas : 1;
+      const int64_t need = ((ba.hi - ba.lo) + cpc - 1) / cpc;
+      int64_t grid = b.grid / unit;
+      if (grid > need) grid = need;
+      if (grid < 1) grid = 1;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (c->opt.profile) {
+        e0 = get_event(c);
+        e1 = get_event(c);
+        cudaEventRecord(e0, s);
+      }
+      void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
+      void *args[] = {&a, &ba};
+      SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)(grid * unit)), dim3(b.block), args, 0, s));
+      ++c->launches;
+      if (c->opt.profile) {
+        cudaEventRecord(e1, s);
+        c->ev_pending.push_back({i, {e0, e1}});
+      }
     }
   }
   return SCD_OK;

@@ -76,53 +76,59 @@ __global__ void k_gather_t(const int64_t *perm, const int32_t *outer_of, const f
 }
 
 // s[idx[k]] += |val[k]|  (s = |A|ᵀ1 for CSR, |A|1 for CSC), fp64
-__global__ void k_abs_scatter(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, double *s) {
+// s[idx[k]] += |val[k]| over the coordinates of a bin (s = |A_b|ᵀ1 for CSR, |A_b|1 for CSC), fp64;
+// acc[1] += Σ_bin ||a||² (from the fp32 norms)
+__global__ void k_abs_scatter(const int64_t *ptr, const int32_t *idx, const float *val, const int32_t *list,
+                              int64_t count, const float *norm, double *s, double *acc) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t o = warp; o < outer; o += nwarps)
+  for (int64_t j = warp; j < count; j += nwarps) {
+    const int64_t o = list ? list[j] : j;
     for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) atomicAdd(s + idx[k], (double)fabsf(val[k]));
+    if (lane == 0) atomicAdd(acc + 1, (double)norm[o]);
+  }
 }
-// acc[0] += Σ s_i², acc[1] += Σ norm_o
-__global__ void __launch_bounds__(256) k_coupling_sums(const double *s, int64_t n, const float *norm, int64_t nc,
-                                                       double *acc) {
-  double a = 0.0, b = 0.0;
+// acc[0] += Σ s_i²
+__global__ void __launch_bounds__(256) k_sumsq(const double *s, int64_t n, double *acc) {
+  double a = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     a += s[i] * s[i];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
-    b += (double)norm[i];
   block_sum_atomic<256>(a, acc + 0);
-  block_sum_atomic<256>(b, acc + 1);
+}
+
+// Fraction of the estimated staleness bound used as the default in-flight cap;
+// SCD_CAP_FRACTION overrides it for tuning experiments (tools/sweep_inflight.py).
+double cap_fraction() {
+  const char *e = getenv("SCD_CAP_FRACTION");
+  double f = e ? atof(e) : 0.5;
+  return f > 0 ? f : 0.5;
 }
 
 }  // namespace
 
-// Staleness bound for the asynchronous kernels.  With τ coordinates in flight a
-// coordinate's update sees up to τ concurrent updates it did not read.  Treating them as one
-// block-Jacobi step, the step stays contractive while τ·c̄ < λN + d̄ (diagonal dominance of the
-// coordinate Hessian block), where d̄ = mean ||a||² and c̄ = mean |<a_i, a_j>| over coordinate
-// pairs, estimated here from ||(|A|ᵀ1)||² = Σ_i Σ_j |<a_i,a_j>| (upper bound of the mean |.|).
-scd_status estimate_inflight_cap(scd_ctx *c) {
+// Staleness bound for one bin of the asynchronous schedule.  With τ coordinates of
+// the bin in flight, a coordinate's update misses up to τ-1 concurrent updates.  Treating them as
+// one block-Jacobi step, the step stays contractive while τ·c̄ < λN + d̄ (diagonal dominance of the
+// coordinate-Hessian block), with d̄ = mean ||a||² and c̄ = mean |<a_i, a_j>| over pairs of the bin,
+// obtained from ||(|A_b|ᵀ1)||² = Σ_i Σ_j |<a_i,a_j>| (so c̄ upper-bounds the mean |<a_i,a_j>|).
+// Bins run one after another, so only intra-bin concurrency matters.
+scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau) {
   cudaStream_t s = c->stream;
   double *vec = c->vec64;
   SCD_CK(c, cudaMemsetAsync(vec, 0, sizeof(double) * (size_t)c->n_shared, s));
   SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 2, s));
-  k_abs_scatter<<<grid_for(c->n_coord * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, c->n_coord, vec);
-  k_coupling_sums<<<grid_for(c->n_shared > c->n_coord ? c->n_shared : c->n_coord, 256, 148 * 8), 256, 0, s>>>(
-      vec, c->n_shared, c->norm, c->n_coord, c->acc);
+  k_abs_scatter<<<grid_for(count * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, d_list, count, c->norm, vec,
+                                                                    c->acc);
+  k_sumsq<<<grid_for(c->n_shared, 256, 148 * 8), 256, 0, s>>>(vec, c->n_shared, c->acc);
   SCD_CKL(c, "coupling estimate");
   double h[2];
   SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(h), cudaMemcpyDeviceToHost, s));
   SCD_CK(c, cudaStreamSynchronize(s));
-  const double n = (double)(c->n_nonempty > 1 ? c->n_nonempty : 2);
-  const double cbar = (h[0] - h[1]) / (n * (n - 1.0));  // mean off-diagonal |<a_i, a_j>| (upper bound)
+  const double n = (double)(count > 1 ? count : 2);
+  const double cbar = (h[0] - h[1]) / (n * (n - 1.0));
   const double dbar = h[1] / n + c->lamN;
-  double tau = cbar > 0 ? dbar / cbar : 1e18;
-  c->tau_star = tau;
-  double cap = 0.5 * tau;
-  if (cap < 32) cap = 32;
-  if (cap > 1e9) cap = 1e9;
-  c->auto_cap = (int64_t)cap;
+  *tau = cbar > 0 ? dbar / cbar : 1e18;
   return SCD_OK;
 }
 
@@ -154,18 +160,20 @@ scd_status build_schedule(scd_ctx *c) {
   std::vector<int64_t> hp((size_t)n + 1);
   SCD_CK(c, cudaMemcpyAsync(hp.data(), c->ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost, c->stream));
   SCD_CK(c, cudaStreamSynchronize(c->stream));
-  // bin thresholds (entries per coordinate): (0,64] -> 8-lane groups, (64,1024] -> warps, >1024 -> CTA
-  const int64_t lim[3] = {64, 1024, INT64_MAX};
-  const int lanes[3] = {8, 32, 256};
-  std::vector<int32_t> lists[3], empty;
-  int64_t nnzb[3] = {0, 0, 0};
+  // bin thresholds (entries per coordinate): (0,64] -> 8-lane groups, (64,1024] -> warps,
+  // (1024,16384] -> one CTA, > 16384 -> one 8-CTA cluster per coordinate
+  constexpr int NB = 4;
+  const int64_t lim[NB] = {64, 1024, 16384, INT64_MAX};
+  const int lanes[NB] = {8, 32, kLanesCta, kLanesCluster};
+  std::vector<int32_t> lists[NB], empty;
+  int64_t nnzb[NB] = {0, 0, 0, 0};
   for (int64_t i = 0; i < n; ++i) {
     const int64_t L = hp[(size_t)i + 1] - hp[(size_t)i];
     if (L == 0) {
       empty.push_back((int32_t)i);
       continue;
     }
-    for (int b = 0; b < 3; ++b)
+    for (int b = 0; b < NB; ++b)
       if (L <= lim[b]) {
         lists[b].push_back((int32_t)i);
         nnzb[b] += L;
@@ -178,13 +186,10 @@ scd_status build_schedule(scd_ctx *c) {
     SCD_CK(c, cudaMalloc((void **)&c->empty_list, sizeof(int32_t) * empty.size()));
     SCD_CK(c, cudaMemcpy(c->empty_list, empty.data(), sizeof(int32_t) * empty.size(), cudaMemcpyHostToDevice));
   }
-  scd_status st = estimate_inflight_cap(c);
-  if (st != SCD_OK) return st;
-  // launch order: long coordinates first (CTA), then warps, then 8-lane groups
+  // launch order: longest coordinates first
   c->n_bins = 0;
-  const int order[3] = {2, 1, 0};
-  for (int oi = 0; oi < 3; ++oi) {
-    const int b = order[oi];
+  c->tau_star = 1e18;
+  for (int b = NB - 1; b >= 0; --b) {
     if (lists[b].empty()) continue;
     Bin &B = c->bins[c->n_bins];
     B.lanes = lanes[b];
@@ -197,10 +202,21 @@ scd_status build_schedule(scd_ctx *c) {
       SCD_CK(c, cudaMalloc((void **)&B.list, sizeof(int32_t) * lists[b].size()));
       SCD_CK(c, cudaMemcpy(B.list, lists[b].data(), sizeof(int32_t) * lists[b].size(), cudaMemcpyHostToDevice));
     }
+    scd_status st = estimate_bin_tau(c, B.list, B.count, &B.tau);
+    if (st != SCD_OK) return st;
+    if (B.tau < c->tau_star) c->tau_star = B.tau;
+    double cap = cap_fraction() * B.tau;
+    B.cap = c->opt.max_inflight > 0 ? (int64_t)c->opt.max_inflight : (int64_t)(cap < 1 ? 1 : (cap > 1e9 ? 1e9 : cap));
     bin_launch_shape(c, B);
     ++c->n_bins;
   }
-  SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * kMaxBins));
+  // interleave the bins in slices when more than one bin carries work (reading c24)
+  c->n_slices = c->n_bins > 1 ? 8 : 1;
+  if (const char *e = getenv("SCD_SLICES")) {
+    int v = atoi(e);
+    if (v >= 1 && v <= kMaxSlices) c->n_slices = v;
+  }
+  SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * kMaxBins * kMaxSlices));
   return SCD_OK;
 }
 

@@ -222,10 +222,11 @@ def test_async_converges_to_oracle_optimum(c2full, form):
 
 def test_async_short_rows_group_kernel():
     """Criteo-shaped rows (39 one-hot fields) run on the 8-lane group kernel."""
-    cfg = synth.c5_scaled(30_000, 1e-3)
+    cfg = synth.c5_scaled(200_000, 1e-2)
     d = synth.gen_host(cfg)
     pr = solver.Problem.from_csr(d)
     s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=1)
+    print("schedule", s.info())
     assert s.info()["bins"][0]["lanes"] == 8
     xs, _, hist = solver.solve(pr, "dual", 15, seed=1)
     for t in range(1, 16):
