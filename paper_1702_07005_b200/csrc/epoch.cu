@@ -35,6 +35,7 @@ struct EpochArgs {
   float *x;
   float *sv;
   double lam, lamN;
+  int exp_flags;  // measurement experiments only (SCD_EXPERIMENT): 1 = no scatter, 2 = no gather
 };
 
 struct BinArgs {
@@ -60,6 +61,27 @@ __device__ __forceinline__ float scatter_scale(float d) { return FORM == SCD_PRI
 __device__ __forceinline__ float ld_sv(const float *p) { return __ldcg(p); }
 __device__ __forceinline__ void red_add(float *p, float v) { atomicAdd(p, v); }  // RED.E.ADD.F32
 
+// Atomic scatter of the entries k = k0 + j*stride (k < end) of a coordinate, U entries at a time
+// with all their (idx, val) loads issued before the REDs (the compiler may not hoist loads above
+// a RED it cannot prove does not alias them, which would serialise one L2 round trip per entry).
+template <int U>
+__device__ __forceinline__ void scatter_strided(float *sv, const int32_t *idx, const float *val, int64_t k0,
+                                                int64_t end, int64_t stride, float d) {
+  for (int64_t k = k0; k < end; k += stride * U) {
+    int32_t id[U];
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t kk = k + (int64_t)u * stride;
+      id[u] = kk < end ? __ldcg(idx + kk) : -1;
+      v[u] = kk < end ? __ldcg(val + kk) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (id[u] >= 0) red_add(sv + id[u], v[u] * d);
+  }
+}
+
 __device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
   uint64_t j = perm_apply(b.perm, t);
   return b.list ? (int64_t)__ldg(b.list + j) : (int64_t)j;
@@ -74,8 +96,8 @@ __device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
 // variant below ran at 50% occupancy and was latency-bound).  Thread 0 software-pipelines the
 // schedule: the next ticket's atomic is issued before pass 1 and its coordinate / offsets are
 // fetched before pass 2, so neither latency sits on the critical path.
-template <int FORM, int T, int U>
-__global__ void __launch_bounds__(T, 2048 / T) k_epoch_stream(EpochArgs a, BinArgs b) {
+template <int FORM, int T, int U, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b) {
   constexpr int NW = T / 32;
   __shared__ float s_red[NW];
   __shared__ float s_delta;
@@ -103,6 +125,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_epoch_stream(EpochArgs a, BinAr
     const long long c = s_c;
     if (c < 0) break;
     const int64_t beg = s_beg, end = s_end;
+    if ((a.exp_flags & 4) && tid == 0) asm volatile("fence.acquire.gpu;" ::: "memory");  // CCTL.IVALL: drop stale L1 lines
     float xc = 0.f, nrm = 0.f, yc = 0.f;
     if (tid == 0) {  // consumed after the reduction
       xc = a.x[c];
@@ -122,7 +145,9 @@ __global__ void __launch_bounds__(T, 2048 / T) k_epoch_stream(EpochArgs a, BinAr
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (id[u] >= 0) acc = fmaf(ld_sv(a.sv + id[u]), v[u], acc);
+        if (id[u] >= 0)
+          acc = fmaf((a.exp_flags & 2) ? (float)id[u] : ((a.exp_flags & 4) ? __ldca(a.sv + id[u]) : ld_sv(a.sv + id[u])),
+                     v[u], acc);
     }
     if (tid == 0) {  // schedule the next coordinate while the block reduces / scatters
       const int64_t t = b.lo + (int64_t)nticket;
@@ -147,13 +172,21 @@ __global__ void __launch_bounds__(T, 2048 / T) k_epoch_stream(EpochArgs a, BinAr
     }
     __syncthreads();
     const float d = scatter_scale<FORM>(s_delta);
-    if (d != 0.f) {
+    if (d != 0.f && !(a.exp_flags & 1)) {
       for (int64_t base = beg + tid; base < end; base += (int64_t)T * U) {
+        // all U (idx, val) loads first: the REDs may alias them as far as the compiler knows,
+        // so interleaving would serialise one L2 round trip per entry
+        int32_t id[U];
+        float v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t k = base + (int64_t)u * T;
-          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
+          id[u] = k < end ? __ldcg(a.idx + k) : -1;
+          v[u] = k < end ? __ldcg(a.val + k) : 0.f;
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (id[u] >= 0) red_add(a.sv + id[u], v[u] * d);
       }
     }
   }
@@ -222,13 +255,7 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
 #pragma unroll
       for (int e = 0; e < E; ++e)
         if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
-#pragma unroll 4
-        for (int e = 0; e < E; ++e) {
-          const int64_t k = base + (int64_t)e * T + tid;
-          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
-        }
-      }
+      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
     }
   }
 }
@@ -291,13 +318,7 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
 #pragma unroll
       for (int e = 0; e < E; ++e)
         if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      for (int64_t base = beg + (int64_t)G * E; base < end; base += (int64_t)G * E) {
-#pragma unroll 4
-        for (int e = 0; e < E; ++e) {
-          const int64_t k = base + (int64_t)e * G + gl;
-          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
-        }
-      }
+      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
     }
   }
 }
@@ -440,13 +461,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
 #pragma unroll
       for (int e = 0; e < E; ++e)
         if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
-#pragma unroll 4
-        for (int e = 0; e < E; ++e) {
-          const int64_t k = base + (int64_t)e * T + tid;
-          if (k < end) red_add(a.sv + __ldcg(a.idx + k), __ldcg(a.val + k) * d);
-        }
-      }
+      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
     }
   }
 }
@@ -464,7 +479,11 @@ void *kernel_for(int lanes) {
     case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE>;
     default: {
       static const bool regs = getenv("SCD_CTA_KERNEL") && std::string(getenv("SCD_CTA_KERNEL")) == "regs";
-      return regs ? (void *)k_epoch_cta<FORM, kCtaT, kCtaE> : (void *)k_epoch_stream<FORM, kCtaT, kStreamU>;
+      static const int var = getenv("SCD_STREAM_VARIANT") ? atoi(getenv("SCD_STREAM_VARIANT")) : 0;
+      if (regs) return (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
+      if (var == 1) return (void *)k_epoch_stream<FORM, kCtaT, 8, 6>;
+      if (var == 2) return (void *)k_epoch_stream<FORM, 512, 4, 4>;
+      return (void *)k_epoch_stream<FORM, kCtaT, kStreamU, 8>;
     }
   }
 }
@@ -480,6 +499,8 @@ EpochArgs make_args(scd_ctx *c) {
   a.sv = c->sv;
   a.lam = c->lam;
   a.lamN = c->lamN;
+  static const int ef = getenv("SCD_EXPERIMENT") ? atoi(getenv("SCD_EXPERIMENT")) : 0;
+  a.exp_flags = ef;
   return a;
 }
 
@@ -502,7 +523,8 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
   const bool group = (b.lanes == 8 || b.lanes == 32);
   const bool clus = (b.lanes == kLanesCluster);
-  int block = group ? 256 : (clus ? kClusterThreads : kCtaT);
+  const bool v512 = getenv("SCD_STREAM_VARIANT") && atoi(getenv("SCD_STREAM_VARIANT")) == 2;
+  int block = group ? 256 : (clus ? kClusterThreads : (v512 ? 512 : kCtaT));
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
   if (group && b.cap > 0 && b.cap * b.lanes < block) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
