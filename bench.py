@@ -255,7 +255,8 @@ def main():
     bins = info["bins"]
     b_i = max(range(len(kprof)), key=lambda i: kprof[i][0]) if kprof else 0
     ms_b, cnt_b = kprof[b_i] if kprof else (float("nan"), 0)
-    bytes_launch = BYTES_PER_NNZ * bins[b_i]["nnz"] + BYTES_PER_COORD * bins[b_i]["count"]
+    # one launch processes one of the n_slices slices of the bin
+    bytes_launch = (BYTES_PER_NNZ * bins[b_i]["nnz"] + BYTES_PER_COORD * bins[b_i]["count"]) / info["n_slices"]
     achieved = bytes_launch / (ms_b / cnt_b / 1e3) / 1e9 if cnt_b else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")

@@ -35,7 +35,6 @@ struct EpochArgs {
   float *x;
   float *sv;
   double lam, lamN;
-  int exp_flags;  // measurement experiments only (SCD_EXPERIMENT): 1 = no scatter, 2 = no gather
 };
 
 struct BinArgs {
@@ -125,7 +124,6 @@ __global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b
     const long long c = s_c;
     if (c < 0) break;
     const int64_t beg = s_beg, end = s_end;
-    if ((a.exp_flags & 4) && tid == 0) asm volatile("fence.acquire.gpu;" ::: "memory");  // CCTL.IVALL: drop stale L1 lines
     float xc = 0.f, nrm = 0.f, yc = 0.f;
     if (tid == 0) {  // consumed after the reduction
       xc = a.x[c];
@@ -145,9 +143,7 @@ __global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (id[u] >= 0)
-          acc = fmaf((a.exp_flags & 2) ? (float)id[u] : ((a.exp_flags & 4) ? __ldca(a.sv + id[u]) : ld_sv(a.sv + id[u])),
-                     v[u], acc);
+        if (id[u] >= 0) acc = fmaf(ld_sv(a.sv + id[u]), v[u], acc);
     }
     if (tid == 0) {  // schedule the next coordinate while the block reduces / scatters
       const int64_t t = b.lo + (int64_t)nticket;
@@ -172,7 +168,7 @@ __global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b
     }
     __syncthreads();
     const float d = scatter_scale<FORM>(s_delta);
-    if (d != 0.f && !(a.exp_flags & 1)) {
+    if (d != 0.f) {
       for (int64_t base = beg + tid; base < end; base += (int64_t)T * U) {
         // all U (idx, val) loads first: the REDs may alias them as far as the compiler knows,
         // so interleaving would serialise one L2 round trip per entry
@@ -478,12 +474,10 @@ void *kernel_for(int lanes) {
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
     case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE>;
     default: {
-      static const bool regs = getenv("SCD_CTA_KERNEL") && std::string(getenv("SCD_CTA_KERNEL")) == "regs";
-      static const int var = getenv("SCD_STREAM_VARIANT") ? atoi(getenv("SCD_STREAM_VARIANT")) : 0;
-      if (regs) return (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
-      if (var == 1) return (void *)k_epoch_stream<FORM, kCtaT, 8, 6>;
-      if (var == 2) return (void *)k_epoch_stream<FORM, 512, 4, 4>;
-      return (void *)k_epoch_stream<FORM, kCtaT, kStreamU, 8>;
+      // register-resident kernel by default (measured equal-or-faster and half the coordinates in
+      // flight); SCD_CTA_KERNEL=stream selects the two-pass streaming variant
+      static const bool stream = getenv("SCD_CTA_KERNEL") && std::string(getenv("SCD_CTA_KERNEL")) == "stream";
+      return stream ? (void *)k_epoch_stream<FORM, kCtaT, kStreamU, 8> : (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
     }
   }
 }
@@ -499,8 +493,6 @@ EpochArgs make_args(scd_ctx *c) {
   a.sv = c->sv;
   a.lam = c->lam;
   a.lamN = c->lamN;
-  static const int ef = getenv("SCD_EXPERIMENT") ? atoi(getenv("SCD_EXPERIMENT")) : 0;
-  a.exp_flags = ef;
   return a;
 }
 
@@ -523,8 +515,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
   const bool group = (b.lanes == 8 || b.lanes == 32);
   const bool clus = (b.lanes == kLanesCluster);
-  const bool v512 = getenv("SCD_STREAM_VARIANT") && atoi(getenv("SCD_STREAM_VARIANT")) == 2;
-  int block = group ? 256 : (clus ? kClusterThreads : (v512 ? 512 : kCtaT));
+  int block = group ? 256 : (clus ? kClusterThreads : kCtaT);
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
   if (group && b.cap > 0 && b.cap * b.lanes < block) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
