@@ -165,6 +165,9 @@ typedef struct {
   int64_t bin_cap[4];     /* per bin: coordinates in flight allowed (max_inflight, else bin_tau/2) */
   double bin_tau[4];      /* per bin: estimated staleness bound */
   int32_t n_slices;       /* the bins are interleaved in this many slices per epoch (reading c24) */
+  int64_t sv_offset_bytes;/* placement of the shared vector chosen at create */
+  float probe_best_ms;    /* placement probe: fastest / slowest candidate (0 if not probed) */
+  float probe_worst_ms;
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

@@ -48,7 +48,7 @@ void free_ctx(scd_ctx *c) {
   cudaFree(c->own_y);
   cudaFree(c->x);
   cudaFree(c->x0);
-  cudaFree(c->sv);
+  cudaFree(c->sv_base);
   cudaFree(c->sv0);
   cudaFree(c->norm);
   cudaFree(c->empty_list);
@@ -192,15 +192,34 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
   }
   if ((st = dev_alloc(c, &c->x, c->n_coord, "alloc model")) != SCD_OK) return bail(st);
   if ((st = dev_alloc(c, &c->x0, c->n_coord, "alloc model snapshot")) != SCD_OK) return bail(st);
-  if ((st = dev_alloc(c, &c->sv, c->n_shared, "alloc shared")) != SCD_OK) return bail(st);
+  // the shared vector sits at a tuned offset inside a slightly larger allocation (tune_shared_layout)
+  if ((st = dev_alloc(c, &c->sv_base, c->n_shared + kMaxSvOffsetFloats, "alloc shared")) != SCD_OK) return bail(st);
+  c->sv = c->sv_base;
   if ((st = dev_alloc(c, &c->sv0, c->n_shared, "alloc shared snapshot")) != SCD_OK) return bail(st);
   if ((st = dev_alloc(c, &c->norm, c->n_coord, "alloc norms")) != SCD_OK) return bail(st);
   if ((st = dev_alloc(c, &c->acc, 32, "alloc acc")) != SCD_OK) return bail(st);
   if ((st = dev_alloc(c, &c->vec64, c->n_shared, "alloc vec64")) != SCD_OK) return bail(st);
   if ((st = dev_alloc(c, &c->comm, c->n_shared, "alloc comm")) != SCD_OK) return bail(st);
-  // initial state (Alg. 1/2 "Initialize: β = 0, w = 0"): model 0; primal residual r = y - 0 = y; w̄ = 0
   cudaMemsetAsync(c->x, 0, sizeof(float) * (size_t)c->n_coord, s);
   cudaMemsetAsync(c->x0, 0, sizeof(float) * (size_t)c->n_coord, s);
+  if ((st = compute_norms(c)) != SCD_OK) return bail(st);
+  if ((st = build_schedule(c)) != SCD_OK) return bail(st);
+  {
+    // shared-vector placement: SCD_SV_OFFSET (bytes) pins it; otherwise large asynchronous
+    // problems are probed (tune_shared_layout); SCD_SV_TUNE=0 disables the probe
+    const char *e = getenv("SCD_SV_OFFSET");
+    const char *tn = getenv("SCD_SV_TUNE");
+    if (e) {
+      int64_t off = (atoll(e) / 16) * 4;
+      if (off < 0) off = 0;
+      if (off > kMaxSvOffsetFloats) off = kMaxSvOffsetFloats;
+      c->sv = c->sv_base + off;
+      c->sv_offset_bytes = off * 4;
+    } else if (!opt.deterministic && c->n_bins > 0 && c->nnz >= (int64_t)20000000 && !(tn && atoi(tn) == 0)) {
+      if ((st = tune_shared_layout(c)) != SCD_OK) return bail(st);
+    }
+  }
+  // initial state (Alg. 1/2 "Initialize: β = 0, w = 0"): model 0; primal residual r = y - 0 = y; w̄ = 0
   if (form == SCD_PRIMAL) {
     cudaMemcpyAsync(c->sv, c->y, sizeof(float) * (size_t)c->n_shared, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(c->sv0, c->y, sizeof(float) * (size_t)c->n_shared, cudaMemcpyDeviceToDevice, s);
@@ -208,8 +227,6 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
     cudaMemsetAsync(c->sv, 0, sizeof(float) * (size_t)c->n_shared, s);
     cudaMemsetAsync(c->sv0, 0, sizeof(float) * (size_t)c->n_shared, s);
   }
-  if ((st = compute_norms(c)) != SCD_OK) return bail(st);
-  if ((st = build_schedule(c)) != SCD_OK) return bail(st);
   // the all-zero start is already the fixed point of every empty coordinate (Δ = -β = 0 primal);
   // the dual's empty rows still move (α_n = y_n/N), so they run in the first epoch.
   c->empty_dirty = (form == SCD_DUAL);
@@ -331,6 +348,13 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->launches = c->launches;
   info->tau_star = c->tau_star;
   info->n_slices = c->n_slices;
+  info->sv_offset_bytes = c->sv_offset_bytes;
+  info->probe_best_ms = 0.f;
+  info->probe_worst_ms = 0.f;
+  for (int i = 0; i < c->n_probe; ++i) {
+    if (i == 0 || c->probe_ms[i] < info->probe_best_ms) info->probe_best_ms = c->probe_ms[i];
+    if (c->probe_ms[i] > info->probe_worst_ms) info->probe_worst_ms = c->probe_ms[i];
+  }
   info->inflight_cap = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i) {
     info->bin_cap[i] = c->bins[i].cap;

@@ -14,6 +14,11 @@ namespace scd {
 
 constexpr int kMaxBins = 4;
 constexpr int kMaxSlices = 64;
+// shared-vector placement candidates (bytes into its allocation), epoch.cu tune_shared_layout
+constexpr int kSvCandidates = 18;
+constexpr int64_t kSvCandidateBytes[kSvCandidates] = {0,     4096,  8192,  12288, 16384, 20480,  24576,  28672, 32768,
+                                                      36864, 40960, 45056, 49152, 53248, 57344, 61440, 131072, 262144};
+constexpr int64_t kMaxSvOffsetFloats = 262144 / 4;
 constexpr uint32_t kPartStream = 0x50415254u;  // "PART": partition permutation stream (c15)
 
 // ------------------------------------------------------------------------------------------
@@ -110,6 +115,10 @@ struct scd_ctx {
   // model and shared vector (fp32) plus aggregation base point snapshots
   float *x = nullptr, *x0 = nullptr;    // β (primal) / α (dual)  [n_coord]
   float *sv = nullptr, *sv0 = nullptr;  // r = y - Aβ (primal) / w̄ = Aᵀα (dual)  [n_shared]
+  float *sv_base = nullptr;             // allocation holding sv (sv may sit at an offset in it)
+  int64_t sv_offset_bytes = 0;          // chosen placement of sv in sv_base
+  int n_probe = 0;                      // placement probe times (ms) per candidate
+  float probe_ms[32] = {0};
   float *norm = nullptr;                // ||a_m||² / ||ā_n||²  [n_coord]
   // asynchronous schedule
   int n_bins = 0;
@@ -169,6 +178,7 @@ scd_status transpose_device(const int64_t *ptr, const int32_t *idx, const float 
 // epoch.cu -------------------------------------------------------------------------------------
 scd_status run_epoch(scd_ctx *c, uint32_t epoch);
 scd_status profile_collect(scd_ctx *c);
+scd_status tune_shared_layout(scd_ctx *c);
 void bin_launch_shape(scd_ctx *c, Bin &b);
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
 scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);

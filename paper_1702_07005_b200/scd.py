@@ -45,7 +45,8 @@ class Info(C.Structure):
                 ("n_bins", C.c_int32), ("bin_kind", C.c_int32 * 4), ("bin_count", C.c_int64 * 4),
                 ("bin_nnz", C.c_int64 * 4), ("bin_grid", C.c_int32 * 4), ("bin_block", C.c_int32 * 4),
                 ("launches", C.c_int64), ("tau_star", C.c_double), ("inflight_cap", C.c_int64),
-                ("bin_cap", C.c_int64 * 4), ("bin_tau", C.c_double * 4), ("n_slices", C.c_int32)]
+                ("bin_cap", C.c_int64 * 4), ("bin_tau", C.c_double * 4), ("n_slices", C.c_int32),
+                ("sv_offset_bytes", C.c_int64), ("probe_best_ms", C.c_float), ("probe_worst_ms", C.c_float)]
 
 
 _lib = None
@@ -216,7 +217,8 @@ class Solver:
         nb = inf.n_bins
         return dict(n_coord=inf.n_coord, n_shared=inf.n_shared, nnz=inf.nnz, n_nonempty=inf.n_nonempty,
                     launches=inf.launches, tau_star=inf.tau_star, inflight_cap=inf.inflight_cap,
-                    n_slices=inf.n_slices,
+                    n_slices=inf.n_slices, sv_offset_bytes=inf.sv_offset_bytes,
+                    probe_ms=(inf.probe_best_ms, inf.probe_worst_ms),
                     bins=[dict(lanes=inf.bin_kind[i], count=inf.bin_count[i], nnz=inf.bin_nnz[i],
                                grid=inf.bin_grid[i], block=inf.bin_block[i], cap=inf.bin_cap[i],
                                tau=inf.bin_tau[i]) for i in range(nb)])

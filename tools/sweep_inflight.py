@@ -27,8 +27,9 @@ def main():
         p, i, v = d["ptr"], d["idx"], d["val"]
     rec = int(sys.argv[5]) if len(sys.argv) > 5 else 0
     for cap in caps:
-        s = scd.Solver(p, i, v, n_rows, n_cols, d["y"], cfg.lam, form, seed=4, max_inflight=max(cap, 0),
-                       profile=True, deterministic=cap < 0, recompute_every=rec)
+        st = torch.cuda.Stream() if os.environ.get("SWEEP_TORCH_STREAM") else None
+        s = scd.Solver(p, i, v, n_rows, n_cols, d["y"], cfg.lam, form, seed=int(os.environ.get("SWEEP_SEED", 4)),
+                       max_inflight=max(cap, 0), profile=True, deterministic=cap < 0, recompute_every=rec, stream=st)
         info = s.info()
         gaps, ms = [], []
         for t in range(1, epochs + 1):
