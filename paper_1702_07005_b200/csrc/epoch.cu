@@ -324,6 +324,132 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
 }
 
 // ----------------------------------------------------------------------------------------------
+// Software-pipelined sub-warp kernel for short coordinates (criteo-shaped rows, 39 entries).
+// With a short coordinate the epoch is bound by its dependent round trips (ticket -> coordinate
+// -> offsets -> entries -> gathers -> delta -> scatter), and the staleness cap limits how many
+// coordinates may be in flight.  So each warp overlaps the next batch's loads with the current
+// batch's compute: while batch i gathers / reduces / scatters, batch i+1's offsets, scalars and
+// entries are already in flight, and batch i+2's coordinates are computed.  Only batch i reads
+// the shared vector, so prefetching does not add staleness.  Tickets are taken TB batches at a
+// time (one atomic per TB·32/G coordinates).
+template <int FORM, int G, int E, int TB>
+__global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b) {
+  constexpr int CPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / G, gl = lane % G;
+  const unsigned FULL = 0xffffffffu;
+  unsigned int grab = 0, left = 0;
+  // warp-uniform: position of the next batch (or -1 when the slice is exhausted)
+  auto next_pos = [&]() -> int64_t {
+    if (left == 0) {
+      unsigned int g = 0;
+      if (lane == 0) g = atomicAdd(b.counter, (unsigned)(CPW * TB));
+      grab = __shfl_sync(FULL, g, 0);
+      left = TB;
+    }
+    const int64_t t = b.lo + (int64_t)grab + (int64_t)(TB - left) * CPW;
+    --left;
+    return t < b.hi ? t : -1;
+  };
+  // coordinate of this lane's group for the batch at position t (lanes < CPW evaluate the permutation)
+  auto coord_of = [&](int64_t t) -> int64_t {
+    int64_t cl = -1;
+    if (t >= 0 && lane < CPW && t + lane < b.hi) cl = bin_coord(b, (uint64_t)(t + lane));
+    return __shfl_sync(FULL, cl, sub);
+  };
+  // batch i (current) and i+1 (next) state
+  int64_t c_cur = coord_of(next_pos());
+  if (__all_sync(FULL, c_cur < 0)) return;
+  int64_t beg = 0, end = 0;
+  float xc = 0.f, nrm = 0.f, yc = 0.f;
+  if (c_cur >= 0) {
+    beg = __ldg(a.ptr + c_cur);
+    end = __ldg(a.ptr + c_cur + 1);
+    if (gl == 0) {
+      xc = a.x[c_cur];
+      nrm = __ldg(a.norm + c_cur);
+      if (FORM == SCD_DUAL) yc = __ldg(a.y + c_cur);
+    }
+  }
+  int32_t id[E];
+  float v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t k = beg + (int64_t)e * G + gl;
+    id[e] = k < end ? __ldcs(a.idx + k) : -1;
+    v[e] = k < end ? __ldcs(a.val + k) : 0.f;
+  }
+  int64_t c_nxt = coord_of(next_pos());
+  while (!__all_sync(FULL, c_cur < 0)) {
+    // (a) offsets and scalars of batch i+1
+    int64_t nbeg = 0, nend = 0;
+    float nxc = 0.f, nnrm = 0.f, nyc = 0.f;
+    if (c_nxt >= 0) {
+      nbeg = __ldg(a.ptr + c_nxt);
+      nend = __ldg(a.ptr + c_nxt + 1);
+      if (gl == 0) {
+        nxc = a.x[c_nxt];
+        nnrm = __ldg(a.norm + c_nxt);
+        if (FORM == SCD_DUAL) nyc = __ldg(a.y + c_nxt);
+      }
+    }
+    // (b) gather-dot of batch i
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
+    for (int64_t base = beg + (int64_t)G * E; base < end; base += (int64_t)G * E) {
+#pragma unroll 4
+      for (int e = 0; e < E; ++e) {
+        const int64_t k = base + (int64_t)e * G + gl;
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+    // (c) delta of batch i (group leader is the single writer of x[c], c10)
+    float d = 0.f;
+    if (c_cur >= 0 && gl == 0) {
+      d = coord_delta<FORM>(acc, xc, nrm, yc, a.lam, a.lamN);
+      if (!b.dry) a.x[c_cur] = xc + d;
+      if (b.dry) d = 0.f;
+    }
+    d = scatter_scale<FORM>(__shfl_sync(FULL, d, sub * G));
+    // (d) entries of batch i+1
+    int32_t nid[E];
+    float nv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = nbeg + (int64_t)e * G + gl;
+      nid[e] = k < nend ? __ldcs(a.idx + k) : -1;
+      nv[e] = k < nend ? __ldcs(a.val + k) : 0.f;
+    }
+    // (e) scatter of batch i
+    if (d != 0.f || b.dry) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
+      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
+    }
+    // (f) coordinates of batch i+2, rotate
+    const bool more = __any_sync(FULL, c_nxt >= 0);
+    const int64_t c_nn = more ? coord_of(next_pos()) : -1;
+    c_cur = c_nxt;
+    beg = nbeg;
+    end = nend;
+    xc = nxc;
+    nrm = nnrm;
+    yc = nyc;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      id[e] = nid[e];
+      v[e] = nv[e];
+    }
+    c_nxt = c_nn;
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
 // Deterministic (debug) epoch: exactly Alg. 1's order with Alg. 2's arithmetic, one coordinate
 // at a time, fixed reduction tree (strided per-thread partials -> xor-shuffle tree -> 8 warp
 // partials summed in order).  Plain read-modify-write scatter: one coordinate in flight and
@@ -471,10 +597,19 @@ constexpr int kCtaT = kLanesCta, kCtaE = 16, kStreamU = 4;
 constexpr int kGrpE8 = 8, kGrpE32 = 16;
 constexpr int kClE = 8;
 
+// sub-warp bins use the software-pipelined kernel unless SCD_GROUP_KERNEL=plain
+inline bool group_pipe() {
+  static const bool plain = getenv("SCD_GROUP_KERNEL") && std::string(getenv("SCD_GROUP_KERNEL")) == "plain";
+  return !plain;
+}
+
 template <int FORM>
 void *kernel_for(int lanes) {
   switch (lanes) {
-    case 8: return (void *)k_epoch_group<FORM, 8, kGrpE8>;
+    case 8:
+      return group_pipe() ? (void *)k_epoch_group_pipe<FORM, 8, kGrpE8, 4> : (void *)k_epoch_group<FORM, 8, kGrpE8>;
+    case 16:
+      return group_pipe() ? (void *)k_epoch_group_pipe<FORM, 16, 4, 4> : (void *)k_epoch_group<FORM, 16, 4>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
     case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE>;
     default: {
@@ -517,7 +652,7 @@ cudaEvent_t get_event(scd_ctx *c) {
 // kernel's residency, capped by max_inflight coordinates in flight.
 void bin_launch_shape(scd_ctx *c, Bin &b) {
   void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
-  const bool group = (b.lanes == 8 || b.lanes == 32);
+  const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
   int block = group ? 256 : (clus ? kClusterThreads : kCtaT);
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)

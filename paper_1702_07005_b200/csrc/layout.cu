@@ -164,7 +164,11 @@ scd_status build_schedule(scd_ctx *c) {
   // (1024,16384] -> one CTA, > 16384 -> one 8-CTA cluster per coordinate
   constexpr int NB = 4;
   const int64_t lim[NB] = {64, 1024, 16384, INT64_MAX};
-  const int lanes[NB] = {8, 32, kLanesCta, kLanesCluster};
+  int lanes[NB] = {8, 32, kLanesCta, kLanesCluster};
+  if (const char *e = getenv("SCD_SHORT_LANES")) {  // tuning: lanes per short coordinate (8, 16 or 32)
+    const int l = atoi(e);
+    if (l == 8 || l == 16 || l == 32) lanes[0] = l;
+  }
   std::vector<int32_t> lists[NB], empty;
   int64_t nnzb[NB] = {0, 0, 0, 0};
   for (int64_t i = 0; i < n; ++i) {

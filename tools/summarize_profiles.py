@@ -18,12 +18,16 @@ import sys
 from collections import defaultdict
 
 
-def launches(path):
+def launches(path, last=0):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     ki, vi, mi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
     agg = defaultdict(lambda: [0, 0.0])
-    for r in rows[1:]:
+    body = rows[1:]
+    if last:
+        body = body[-last:]
+        print(f"Last {last} launches of the list (the timed region).\n")
+    for r in body:
         if r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki].split("(")[0].replace("<unnamed>::", "").replace("scd::", "")
@@ -95,6 +99,6 @@ def ncu(rep, out_prefix, bytes_per_launch=None):
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        launches(sys.argv[2])
+        launches(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0)
     else:
         ncu(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None)
