@@ -450,6 +450,142 @@ __global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b
 }
 
 // ----------------------------------------------------------------------------------------------
+// CTA-combining sub-warp kernel for short coordinates with heavily shared entries (one-hot
+// criteo-shaped rows: every row carries one of the few values of each small field, so a handful
+// of shared-vector entries receive an atomic from a large fraction of all rows and serialise in
+// their L2 slice).  A CTA processes T/G coordinates per iteration: their entries are inserted into
+// a shared-memory hash table (one slot per distinct index), each distinct entry is gathered ONCE,
+// the coordinates compute their deltas from those values, the scatter is summed per slot with
+// shared-memory atomics, and each distinct entry receives ONE red.global.add.  The T/G
+// coordinates of an iteration are in flight together in every kernel variant (they read before
+// any of them writes), so combining changes rounding order only, not the algorithm.
+template <int FORM, int G, int T, int S>
+__global__ void __launch_bounds__(T) k_epoch_group_comb(EpochArgs a, BinArgs b) {
+  constexpr int E = 64 / G;  // entries per lane: the bin holds coordinates of <= 64 entries
+  constexpr int CPC = T / G;
+  const unsigned FULL = 0xffffffffu;
+  __shared__ int32_t s_key[S];
+  __shared__ float s_g[S];
+  __shared__ float s_r[S];
+  __shared__ int32_t s_list[S];
+  __shared__ int s_n;
+  __shared__ unsigned int s_ticket;
+  // coordinate queue: every QI iterations the whole CTA takes CPC*QI tickets at once, each thread
+  // evaluates one permutation entry and prefetches that coordinate's offsets and scalars (the
+  // single writer of x[c] is this CTA, so the prefetched x[c] is current)
+  constexpr int QI = T / CPC;  // refill = one coordinate per thread
+  __shared__ long long s_qc[T], s_qb[T], s_qe[T];
+  __shared__ float s_qx[T], s_qn[T], s_qy[T];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int grp = tid / G, gl = tid % G, sub = lane / G;
+  for (int i = tid; i < S; i += T) s_key[i] = -1;
+  if (tid == 0) s_n = 0;
+  int qpos = QI;  // iterations consumed from the queue
+  bool more = true;
+  for (;;) {
+    if (qpos == QI) {
+      if (!more) break;
+      if (tid == 0) s_ticket = atomicAdd(b.counter, (unsigned)T);
+      __syncthreads();
+      const int64_t t = b.lo + (int64_t)s_ticket + tid;
+      long long cq = -1, qb = 0, qe = 0;
+      float qx = 0.f, qn = 0.f, qy = 0.f;
+      if (t < b.hi) {
+        cq = bin_coord(b, (uint64_t)t);
+        qb = __ldg(a.ptr + cq);
+        qe = __ldg(a.ptr + cq + 1);
+        qx = a.x[cq];
+        qn = __ldg(a.norm + cq);
+        if (FORM == SCD_DUAL) qy = __ldg(a.y + cq);
+      }
+      s_qc[tid] = cq;
+      s_qb[tid] = qb;
+      s_qe[tid] = qe;
+      s_qx[tid] = qx;
+      s_qn[tid] = qn;
+      s_qy[tid] = qy;
+      more = __syncthreads_or(b.lo + (int64_t)s_ticket + T < b.hi);
+      qpos = 0;
+      if (s_qc[0] < 0) break;  // queue empty (uniform)
+    }
+    const int qi = qpos * CPC + grp;
+    ++qpos;
+    const int64_t c = s_qc[qi];
+    if (__syncthreads_and(c < 0)) {
+      qpos = QI;
+      if (!more) break;
+      continue;
+    }
+    int64_t beg = 0, end = 0;
+    float xc = 0.f, nrm = 0.f, yc = 0.f;
+    if (c >= 0) {
+      beg = s_qb[qi];
+      end = s_qe[qi];
+      xc = s_qx[qi];
+      nrm = s_qn[qi];
+      yc = s_qy[qi];
+    }
+    int32_t slot[E];
+    float v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = beg + (int64_t)e * G + gl;
+      const int32_t id = k < end ? __ldcs(a.idx + k) : -1;
+      v[e] = k < end ? __ldcs(a.val + k) : 0.f;
+      slot[e] = -1;
+      if (id >= 0) {  // insert (linear probing)
+        uint32_t h = ((uint32_t)id * 2654435761u) & (S - 1);
+        for (;;) {
+          const int32_t old = atomicCAS(&s_key[h], -1, id);
+          if (old == -1) {
+            s_list[atomicAdd(&s_n, 1)] = (int32_t)h;
+            break;
+          }
+          if (old == id) break;
+          h = (h + 1) & (S - 1);
+        }
+        slot[e] = (int32_t)h;
+      }
+    }
+    __syncthreads();
+    const int n = s_n;
+    for (int i = tid; i < n; i += T) {  // one gather per distinct entry
+      const int h = s_list[i];
+      s_g[h] = ld_sv(a.sv + s_key[h]);
+      s_r[h] = 0.f;
+    }
+    __syncthreads();
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (slot[e] >= 0) acc = fmaf(s_g[slot[e]], v[e], acc);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+    float d = 0.f;
+    if (c >= 0 && gl == 0) {
+      d = coord_delta<FORM>(acc, xc, nrm, yc, a.lam, a.lamN);
+      if (!b.dry) a.x[c] = xc + d;  // single writer (c10)
+      if (b.dry) d = 0.f;
+    }
+    d = scatter_scale<FORM>(__shfl_sync(FULL, d, sub * G));
+    if (d != 0.f) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (slot[e] >= 0) atomicAdd(&s_r[slot[e]], v[e] * d);
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += T) {  // one atomic per distinct entry
+      const int h = s_list[i];
+      const float r = s_r[h];
+      if (r != 0.f || b.dry) red_add(a.sv + s_key[h], r);
+      s_key[h] = -1;
+    }
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
 // Deterministic (debug) epoch: exactly Alg. 1's order with Alg. 2's arithmetic, one coordinate
 // at a time, fixed reduction tree (strided per-thread partials -> xor-shuffle tree -> 8 warp
 // partials summed in order).  Plain read-modify-write scatter: one coordinate in flight and
@@ -597,19 +733,26 @@ constexpr int kCtaT = kLanesCta, kCtaE = 16, kStreamU = 4;
 constexpr int kGrpE8 = 8, kGrpE32 = 16;
 constexpr int kClE = 8;
 
-// sub-warp bins use the software-pipelined kernel unless SCD_GROUP_KERNEL=plain
-inline bool group_pipe() {
-  static const bool plain = getenv("SCD_GROUP_KERNEL") && std::string(getenv("SCD_GROUP_KERNEL")) == "plain";
-  return !plain;
+// 8-lane bins: 0 = plain, 1 = software-pipelined, 2 = CTA-combining (default); SCD_GROUP_KERNEL
+constexpr int kCombT = 128, kCombS = 2048;
+inline int group_kind() {
+  static const int k = [] {
+    const char *e = getenv("SCD_GROUP_KERNEL");
+    if (!e) return 2;
+    std::string s(e);
+    return s == "plain" ? 0 : (s == "pipe" ? 1 : 2);
+  }();
+  return k;
 }
 
 template <int FORM>
 void *kernel_for(int lanes) {
   switch (lanes) {
     case 8:
-      return group_pipe() ? (void *)k_epoch_group_pipe<FORM, 8, kGrpE8, 4> : (void *)k_epoch_group<FORM, 8, kGrpE8>;
+      if (group_kind() == 2) return (void *)k_epoch_group_comb<FORM, 8, kCombT, kCombS>;
+      return group_kind() == 1 ? (void *)k_epoch_group_pipe<FORM, 8, kGrpE8, 4> : (void *)k_epoch_group<FORM, 8, kGrpE8>;
     case 16:
-      return group_pipe() ? (void *)k_epoch_group_pipe<FORM, 16, 4, 4> : (void *)k_epoch_group<FORM, 16, 4>;
+      return group_kind() == 1 ? (void *)k_epoch_group_pipe<FORM, 16, 4, 4> : (void *)k_epoch_group<FORM, 16, 4>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
     case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE>;
     default: {
@@ -654,9 +797,10 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
   const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
-  int block = group ? 256 : (clus ? kClusterThreads : kCtaT);
+  const bool comb = (b.lanes == 8 && group_kind() == 2);  // fixed CTA size (kernel template)
+  int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : kCtaT));
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
-  if (group && b.cap > 0 && b.cap * b.lanes < block) {
+  if (group && !comb && b.cap > 0 && b.cap * b.lanes < block) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
     if (block < 32) block = 32;
   }

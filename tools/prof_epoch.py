@@ -23,7 +23,8 @@ if form == "primal":
     p, i, v = scd.transpose(p, i, v, d["n_rows"], d["n_cols"], "csr")
 torch.cuda.synchronize()
 t1 = time.perf_counter()
-s = scd.Solver(p, i, v, d["n_rows"], d["n_cols"], d["y"], cfg.lam, form, seed=4, profile="--time" in sys.argv)
+s = scd.Solver(p, i, v, d["n_rows"], d["n_cols"], d["y"], cfg.lam, form, seed=4, profile="--time" in sys.argv,
+               n_global=int(os.environ.get("PROF_NGLOBAL", 0)), max_inflight=int(os.environ.get("PROF_CAP", 0)))
 torch.cuda.synchronize()
 t2 = time.perf_counter()
 print(cfg.name, form, "nnz", s.nnz, "setup %.2fs create %.2fs" % (t1 - t0, t2 - t1), s.info(), flush=True)
