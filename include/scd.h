@@ -55,7 +55,8 @@ typedef enum { SCD_CSR = 0, SCD_CSC = 1 } scd_layout;
 /* Sparse matrix (the local shard of A).  outer = n_rows for CSR, n_cols for CSC.
  *   ptr[outer+1]: ptr[0] = 0, nondecreasing, ptr[outer] = nnz
  *   idx[nnz]    : inner indices in [0, inner), strictly increasing within each outer index
- *   val[nnz]    : values (NULL is rejected in this build: SCD_E_UNSUPPORTED)
+ *   val[nnz]    : values, or NULL = every stored value is 1.0f (one-hot data: the paper's criteo
+ *                 footnote "values ... are always 1 ... could halve the memory usage")
  * Ownership: if mem == SCD_MEM_DEVICE the arrays are BORROWED for the lifetime of the context
  * (the caller keeps them alive and unmodified until scd_destroy; the paper's data "is
  * transferred into the GPU memory once ... and does not move").  If SCD_MEM_HOST the
@@ -188,7 +189,8 @@ scd_status scd_permutation(uint64_t seed, uint32_t epoch, uint32_t stream, int64
 scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_owner_out);
 /* Stable transpose CSR <-> CSC computed on the device.  in->mem says where the input lives;
  * out_mem where ptr_out[inner+1] / idx_out[nnz] / val_out[nnz] (caller-allocated) live.
- * Within each output outer index, entries appear in increasing input-outer order.           */
+ * Within each output outer index, entries appear in increasing input-outer order.
+ * If in->val is NULL (implicit values) only the pattern is transposed and val_out is ignored.  */
 scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out, scd_mem out_mem);
 
 /* ---- NCCL bootstrap helpers (the caller broadcasts the 128-byte id, e.g. via torch.distributed) ---- */

@@ -112,7 +112,6 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
   if ((form == SCD_PRIMAL && A->layout != SCD_CSC) || (form == SCD_DUAL && A->layout != SCD_CSR))
     return fail(nullptr, SCD_E_INVALID_ARG, "primal needs CSC, dual needs CSR");
   if (!A->ptr || (A->nnz > 0 && (!A->idx))) return fail(nullptr, SCD_E_INVALID_ARG, "matrix arrays are NULL");
-  if (!A->val) return fail(nullptr, SCD_E_UNSUPPORTED, "implicit-value matrices (val = NULL) are not supported yet");
   if (A->n_rows > INT32_MAX || A->n_cols > INT32_MAX) return fail(nullptr, SCD_E_UNSUPPORTED, "dimension > 2^31-1");
   scd_options opt;
   scd_default_options(&opt);
@@ -165,12 +164,15 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
     c->own_ptr = p;
     if ((st = dev_alloc(c, &i, A->nnz, "alloc idx")) != SCD_OK) return bail(st);
     c->own_idx = i;
-    if ((st = dev_alloc(c, &v, A->nnz, "alloc val")) != SCD_OK) return bail(st);
-    c->own_val = v;
+    v = nullptr;
+    if (A->val) {  // val == NULL: implicit values 1.0f (NEXT-1), nothing to upload
+      if ((st = dev_alloc(c, &v, A->nnz, "alloc val")) != SCD_OK) return bail(st);
+      c->own_val = v;
+    }
     cudaMemcpyAsync(p, A->ptr, sizeof(int64_t) * (size_t)(outer + 1), cudaMemcpyHostToDevice, s);
     if (A->nnz > 0) {
       cudaMemcpyAsync(i, A->idx, sizeof(int32_t) * (size_t)A->nnz, cudaMemcpyHostToDevice, s);
-      cudaMemcpyAsync(v, A->val, sizeof(float) * (size_t)A->nnz, cudaMemcpyHostToDevice, s);
+      if (A->val) cudaMemcpyAsync(v, A->val, sizeof(float) * (size_t)A->nnz, cudaMemcpyHostToDevice, s);
     }
     c->ptr = p;
     c->idx = i;
@@ -419,8 +421,10 @@ scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_
 
 scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out, scd_mem out_mem) {
   g_err.clear();
-  if (!in || !ptr_out || !in->ptr || (in->nnz > 0 && (!idx_out || !val_out || !in->idx || !in->val)))
+  // in->val == NULL (implicit values) transposes the pattern only; val_out is then ignored
+  if (!in || !ptr_out || !in->ptr || (in->nnz > 0 && (!idx_out || !in->idx || (in->val && !val_out))))
     return fail(nullptr, SCD_E_INVALID_ARG, "NULL argument");
+  const bool has_val = in->val != nullptr;
   const int64_t outer = in->layout == SCD_CSR ? in->n_rows : in->n_cols;
   const int64_t inner = in->layout == SCD_CSR ? in->n_cols : in->n_rows;
   if (outer < 0 || inner < 1 || in->nnz < 0) return fail(nullptr, SCD_E_INVALID_ARG, "bad shape");
@@ -439,12 +443,12 @@ scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_ou
   if (in->mem == SCD_MEM_HOST) {
     alloc(&tp, sizeof(int64_t) * (size_t)(outer + 1));
     alloc(&ti, sizeof(int32_t) * (size_t)nnz);
-    alloc(&tv, sizeof(float) * (size_t)nnz);
+    if (has_val) alloc(&tv, sizeof(float) * (size_t)nnz);
     if (st == SCD_OK) {
       cudaMemcpy(tp, p, sizeof(int64_t) * (size_t)(outer + 1), cudaMemcpyHostToDevice);
       if (nnz) {
         cudaMemcpy(ti, i, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice);
-        cudaMemcpy(tv, v, sizeof(float) * (size_t)nnz, cudaMemcpyHostToDevice);
+        if (has_val) cudaMemcpy(tv, v, sizeof(float) * (size_t)nnz, cudaMemcpyHostToDevice);
       }
       p = (const int64_t *)tp;
       i = (const int32_t *)ti;
@@ -453,11 +457,11 @@ scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_ou
   }
   int64_t *dp = ptr_out;
   int32_t *di = idx_out;
-  float *dv = val_out;
+  float *dv = has_val ? val_out : nullptr;
   if (out_mem == SCD_MEM_HOST) {
     alloc(&op, sizeof(int64_t) * (size_t)(inner + 1));
     alloc(&oi, sizeof(int32_t) * (size_t)nnz);
-    alloc(&ov, sizeof(float) * (size_t)nnz);
+    if (has_val) alloc(&ov, sizeof(float) * (size_t)nnz);
     dp = (int64_t *)op;
     di = (int32_t *)oi;
     dv = (float *)ov;
@@ -471,7 +475,7 @@ scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_ou
     cudaMemcpy(ptr_out, op, sizeof(int64_t) * (size_t)(inner + 1), cudaMemcpyDeviceToHost);
     if (nnz) {
       cudaMemcpy(idx_out, oi, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDeviceToHost);
-      cudaMemcpy(val_out, ov, sizeof(float) * (size_t)nnz, cudaMemcpyDeviceToHost);
+      if (has_val) cudaMemcpy(val_out, ov, sizeof(float) * (size_t)nnz, cudaMemcpyDeviceToHost);
     }
   }
   cudaFree(tp);

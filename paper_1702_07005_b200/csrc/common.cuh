@@ -193,6 +193,13 @@ scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma);
 scd_status aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, double *gamma);
 
 // shared device helpers ------------------------------------------------------------------------
+// Implicit-value matrices (val == nullptr): every stored value is 1.0f — the one-hot case of the
+// paper's criteo footnote ("the values ... are always 1 ... one could halve the memory usage",
+// P:460).  The pointer test is uniform across the grid, so it costs no divergence.
+__device__ __forceinline__ float val_cs(const float *v, int64_t k) { return v ? __ldcs(v + k) : 1.f; }
+__device__ __forceinline__ float val_cg(const float *v, int64_t k) { return v ? __ldcg(v + k) : 1.f; }
+__device__ __forceinline__ float val_at(const float *v, int64_t k) { return v ? v[k] : 1.f; }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -76,7 +76,7 @@ __device__ __forceinline__ void scatter_strided(float *sv, const int32_t *idx, c
     for (int u = 0; u < U; ++u) {
       const int64_t kk = k + (int64_t)u * stride;
       id[u] = kk < end ? __ldcg(idx + kk) : -1;
-      v[u] = kk < end ? __ldcg(val + kk) : 0.f;
+      v[u] = kk < end ? val_cg(val, kk) : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b
       for (int u = 0; u < U; ++u) {
         const int64_t k = base + (int64_t)u * T;
         id[u] = k < end ? __ldcg(a.idx + k) : -1;
-        v[u] = k < end ? __ldcg(a.val + k) : 0.f;
+        v[u] = k < end ? val_cg(a.val, k) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b
         for (int u = 0; u < U; ++u) {
           const int64_t k = base + (int64_t)u * T;
           id[u] = k < end ? __ldcg(a.idx + k) : -1;
-          v[u] = k < end ? __ldcg(a.val + k) : 0.f;
+          v[u] = k < end ? val_cg(a.val, k) : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
       const int64_t k = beg + (int64_t)e * T + tid;
       if (k < end) {
         id[e] = __ldcs(a.idx + k);
-        v[e] = __ldcs(a.val + k);
+        v[e] = val_cs(a.val, k);
       } else {
         id[e] = -1;
         v[e] = 0.f;
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
 #pragma unroll 4
       for (int e = 0; e < E; ++e) {
         const int64_t k = base + (int64_t)e * T + tid;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
       }
     }
     acc = warp_sum(acc);
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
       const int64_t k = beg + (int64_t)e * G + gl;
       if (k < end) {
         id[e] = __ldcs(a.idx + k);
-        v[e] = __ldcs(a.val + k);
+        v[e] = val_cs(a.val, k);
       } else {
         id[e] = -1;
         v[e] = 0.f;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
 #pragma unroll 4
       for (int e = 0; e < E; ++e) {
         const int64_t k = base + (int64_t)e * G + gl;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
       }
     }
 #pragma unroll
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b
   for (int e = 0; e < E; ++e) {
     const int64_t k = beg + (int64_t)e * G + gl;
     id[e] = k < end ? __ldcs(a.idx + k) : -1;
-    v[e] = k < end ? __ldcs(a.val + k) : 0.f;
+    v[e] = k < end ? val_cs(a.val, k) : 0.f;
   }
   int64_t c_nxt = coord_of(next_pos());
   while (!__all_sync(FULL, c_cur < 0)) {
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b
 #pragma unroll 4
       for (int e = 0; e < E; ++e) {
         const int64_t k = base + (int64_t)e * G + gl;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
       }
     }
 #pragma unroll
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b
     for (int e = 0; e < E; ++e) {
       const int64_t k = nbeg + (int64_t)e * G + gl;
       nid[e] = k < nend ? __ldcs(a.idx + k) : -1;
-      nv[e] = k < nend ? __ldcs(a.val + k) : 0.f;
+      nv[e] = k < nend ? val_cs(a.val, k) : 0.f;
     }
     // (e) scatter of batch i
     if (d != 0.f || b.dry) {
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(T) k_epoch_group_comb(EpochArgs a, BinArgs b) 
     for (int e = 0; e < E; ++e) {
       const int64_t k = beg + (int64_t)e * G + gl;
       const int32_t id = k < end ? __ldcs(a.idx + k) : -1;
-      v[e] = k < end ? __ldcs(a.val + k) : 0.f;
+      v[e] = k < end ? val_cs(a.val, k) : 0.f;
       slot[e] = -1;
       if (id >= 0) {  // insert (linear probing)
         uint32_t h = ((uint32_t)id * 2654435761u) & (S - 1);
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kDbgT) k_epoch_debug(EpochArgs a, Perm perm, i
     const int64_t c = (int64_t)perm_apply(perm, (uint64_t)j);
     const int64_t beg = a.ptr[c], end = a.ptr[c + 1];
     float acc = 0.f;
-    for (int64_t k = beg + tid; k < end; k += kDbgT) acc = fmaf(a.sv[a.idx[k]], a.val[k], acc);
+    for (int64_t k = beg + tid; k < end; k += kDbgT) acc = fmaf(a.sv[a.idx[k]], val_at(a.val, k), acc);
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kDbgT) k_epoch_debug(EpochArgs a, Perm perm, i
     }
     __syncthreads();
     const float d = scatter_scale<FORM>(s_delta);
-    for (int64_t k = beg + tid; k < end; k += kDbgT) a.sv[a.idx[k]] += a.val[k] * d;
+    for (int64_t k = beg + tid; k < end; k += kDbgT) a.sv[a.idx[k]] += val_at(a.val, k) * d;
     __syncthreads();
   }
 }
@@ -683,7 +683,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
       const int64_t k = beg + (int64_t)e * T + tid;
       if (k < end) {
         id[e] = __ldcs(a.idx + k);
-        v[e] = __ldcs(a.val + k);
+        v[e] = val_cs(a.val, k);
       } else {
         id[e] = -1;
         v[e] = 0.f;
@@ -696,7 +696,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
 #pragma unroll 4
       for (int e = 0; e < E; ++e) {
         const int64_t k = base + (int64_t)e * T + tid;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), __ldcg(a.val + k), acc);
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
       }
     }
     acc = warp_sum(acc);

@@ -25,7 +25,7 @@ __global__ void k_scatter64(const int64_t *ptr, const int32_t *idx, const float 
   for (int64_t o = warp; o < outer; o += nwarps) {
     const double xo = x[o];
     if (xo == 0.0) continue;
-    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) atomicAdd(out + idx[k], (double)val[k] * xo);
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) atomicAdd(out + idx[k], (double)val_at(val, k) * xo);
   }
 }
 
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kT) k_primal_cols(const int64_t *ptr, const in
   double s_gg = 0.0, s_bb = 0.0, s_g2 = 0.0;
   for (int64_t o = warp; o < outer; o += nwarps) {
     double g = 0.0;
-    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) g += (double)val[k] * res[idx[k]];
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) g += (double)val_at(val, k) * res[idx[k]];
     g = warp_sum(g);
     if (lane == 0) {
       const double b = beta[o];
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kT) k_dual_rows(const int64_t *ptr, const int3
   double s_res = 0.0, s_gg = 0.0, s_aa = 0.0, s_ay = 0.0;
   for (int64_t o = warp; o < outer; o += nwarps) {
     double q = 0.0;
-    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) q += (double)val[k] * v[idx[k]];
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) q += (double)val_at(val, k) * v[idx[k]];
     q = warp_sum(q);
     if (lane == 0) {
       const double a = alpha[o], yo = y[o];

@@ -42,7 +42,7 @@ __global__ void k_norms(const int64_t *ptr, const float *val, int64_t outer, flo
   for (int64_t o = warp; o < outer; o += nwarps) {
     double s = 0.0;
     for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) {
-      const double v = val[k];
+      const double v = val_at(val, k);
       s += v * v;
     }
     s = warp_sum(s);
@@ -71,7 +71,7 @@ __global__ void k_gather_t(const int64_t *perm, const int32_t *outer_of, const f
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = perm[i];
     oidx[i] = outer_of[e];
-    oval[i] = val[e];
+    if (val) oval[i] = val[e];  // implicit-value input -> implicit-value output
   }
 }
 
@@ -85,7 +85,7 @@ __global__ void k_abs_scatter(const int64_t *ptr, const int32_t *idx, const floa
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t j = warp; j < count; j += nwarps) {
     const int64_t o = list ? list[j] : j;
-    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) atomicAdd(s + idx[k], (double)fabsf(val[k]));
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) atomicAdd(s + idx[k], (double)fabsf(val_at(val, k)));
     if (lane == 0) atomicAdd(acc + 1, (double)norm[o]);
   }
 }

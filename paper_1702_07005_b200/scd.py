@@ -142,7 +142,8 @@ class Solver:
             raise ValueError(form)
         p, mp, kp = _buf(ptr, np.int64)
         i, mi, ki = _buf(idx, np.int32)
-        v, mv, kv = _buf(val, np.float32)
+        # val=None: implicit values 1.0f (one-hot data, P:460 footnote)
+        v, mv, kv = _buf(val, np.float32) if val is not None else (None, mp, None)
         if not (mp == mi == mv):
             raise ValueError("ptr/idx/val must all be host arrays or all CUDA tensors")
         yy, my, ky = _buf(y, np.float32)
@@ -272,7 +273,7 @@ def transpose(ptr, idx, val, n_rows: int, n_cols: int, layout: str = "csr"):
     CUDA tensors.  Returns (ptr, idx, val) of the other layout."""
     p, mp, kp = _buf(ptr, np.int64)
     i, mi, ki = _buf(idx, np.int32)
-    v, mv, kv = _buf(val, np.float32)
+    v, mv, kv = _buf(val, np.float32) if val is not None else (None, mp, None)
     lay = CSR if layout == "csr" else CSC
     inner = n_cols if lay == CSR else n_rows
     nnz = int(kp[-1]) if mp == MEM_HOST else int(kp[-1].item())
@@ -285,12 +286,12 @@ def transpose(ptr, idx, val, n_rows: int, n_cols: int, layout: str = "csr"):
         oi = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
         ov = torch.empty(max(nnz, 1), dtype=torch.float32, device=dev)
         _check(lib().scd_transpose(C.byref(m), op.data_ptr(), oi.data_ptr(), ov.data_ptr(), MEM_DEVICE))
-        return op, oi[:nnz], ov[:nnz]
+        return op, oi[:nnz], (ov[:nnz] if v is not None else None)
     op = np.empty(inner + 1, np.int64)
     oi = np.empty(max(nnz, 1), np.int32)
     ov = np.empty(max(nnz, 1), np.float32)
     _check(lib().scd_transpose(C.byref(m), op.ctypes.data, oi.ctypes.data, ov.ctypes.data, MEM_HOST))
-    return op, oi[:nnz], ov[:nnz]
+    return op, oi[:nnz], (ov[:nnz] if v is not None else None)
 
 
 def nccl_unique_id() -> bytes:

@@ -319,3 +319,31 @@ def test_empty_matrix_dual_fixed_point():
     s.epoch(1)
     np.testing.assert_allclose(s.get_model(), y / n, rtol=1e-6)
     assert s.duality_gap() <= 1e-12
+
+
+# ------------------------------------------------------------------ implicit values (NEXT-1)
+@pytest.mark.parametrize("form", ["dual", "primal"])
+def test_implicit_values_equal_explicit_ones(form):
+    """val = NULL (every stored value 1.0f, P:460 footnote) gives bit-identical deterministic epochs,
+    objective and gap to an explicit all-ones value array."""
+    d = synth.gen_host(synth.c5_scaled(3000, 1e-3))
+    assert np.all(d["val"] == 1.0)
+    pr = solver.Problem.from_csr(d)
+    if form == "dual":
+        p, i = d["ptr"], d["idx"]
+    else:
+        p, i, v0 = scd.transpose(d["ptr"], d["idx"], None, pr.N, pr.M, "csr")
+        assert v0 is None and np.array_equal(p, pr.cptr) and np.array_equal(i, pr.cidx)
+    a = scd.Solver(p, i, None, pr.N, pr.M, d["y"], pr.lam, form, seed=2, deterministic=True)
+    b = scd.Solver(p, i, np.ones(len(i), np.float32), pr.N, pr.M, d["y"], pr.lam, form, seed=2, deterministic=True)
+    for t in (1, 2, 3):
+        a.epoch(t)
+        b.epoch(t)
+    assert np.array_equal(a.get_model(), b.get_model())
+    assert a.duality_gap() == b.duality_gap()
+    # asynchronous path too (same schedule; results within async tolerance)
+    c = scd.Solver(_dev(p), _dev(i), None, pr.N, pr.M, _dev(d["y"]), pr.lam, form, seed=2)
+    for t in range(1, 6):
+        c.epoch(t)
+    xs, _, hist = solver.solve(pr, form, 5, seed=2)
+    assert c.duality_gap() <= max(10 * hist[-1]["gap"], 1e-7)

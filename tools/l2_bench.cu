@@ -27,9 +27,13 @@ __global__ void __launch_bounds__(256) k(float *v, unsigned n, unsigned iters, f
 #pragma unroll
       for (int u = 0; u < U; ++u) acc += __ldcg(v + id[u]);
     }
-    if (MODE != 0) {
+    if (MODE == 1 || MODE == 2) {
 #pragma unroll
       for (int u = 0; u < U; ++u) atomicAdd(v + id[u], 1e-9f);
+    }
+    if (MODE == 3) {  // gather from v, RED into a second vector (different lines)
+#pragma unroll
+      for (int u = 0; u < U; ++u) atomicAdd(v + n + id[u], 1e-9f);
     }
   }
   if (acc == 12345.f) sink[0] = acc;
@@ -38,9 +42,9 @@ __global__ void __launch_bounds__(256) k(float *v, unsigned n, unsigned iters, f
 int main(int argc, char **argv) {
   unsigned n = argc > 1 ? atoi(argv[1]) : 680715;
   float *v, *sink;
-  cudaMalloc(&v, sizeof(float) * n);
+  cudaMalloc(&v, sizeof(float) * n * 2);
   cudaMalloc(&sink, 4);
-  cudaMemset(v, 0, sizeof(float) * n);
+  cudaMemset(v, 0, sizeof(float) * n * 2);
   int nsm;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const int grid = nsm * 8, block = 256;
@@ -49,18 +53,19 @@ int main(int argc, char **argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const char *names[3] = {"gather", "red", "gather+red"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char *names[4] = {"gather", "red", "gather+red", "gather+red(2 vectors)"};
+  for (int mode = 0; mode < 4; ++mode) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
       if (mode == 0) k<0, 8><<<grid, block>>>(v, n, iters, sink);
       if (mode == 1) k<1, 8><<<grid, block>>>(v, n, iters, sink);
       if (mode == 2) k<2, 8><<<grid, block>>>(v, n, iters, sink);
+      if (mode == 3) k<3, 8><<<grid, block>>>(v, n, iters, sink);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
-      if (rep == 2) printf("%-11s n=%u: %.1f G elements/s (%.3f ms)\n", names[mode], n, ops / ms / 1e6, ms);
+      if (rep == 2) printf("%-22s n=%u: %.1f G elements/s (%.3f ms)\n", names[mode], n, ops / ms / 1e6, ms);
     }
   }
   return 0;
