@@ -19,6 +19,10 @@ else:
 t0 = time.perf_counter()
 d = synth.gen_device(cfg)
 p, i, v = d["ptr"], d["idx"], d["val"]
+if os.environ.get("PROF_IMPLICIT"):  # one-hot data: drop the all-ones value array (NEXT-1)
+    assert bool((v == 1).all())
+    v = None
+    del d["val"]
 if form == "primal":
     p, i, v = scd.transpose(p, i, v, d["n_rows"], d["n_cols"], "csr")
 torch.cuda.synchronize()
