@@ -85,6 +85,7 @@ struct Bin {
   int lanes = 0;             // lanes per coordinate: 8 / 32 (sub-warp group), 256 (CTA), 4096 (cluster)
   double tau = 0.0;          // estimated staleness bound of the bin (coordinates in flight)
   int64_t cap = 0;           // coordinates in flight allowed
+  int plain = 0;             // 1 = plain sub-warp kernel (cap below the combining kernel's CTA batch)
   int64_t count = 0, nnz = 0;
   int32_t *list = nullptr;   // device, coordinate ids ascending
   int grid = 0, block = 0;

@@ -746,11 +746,11 @@ inline int group_kind() {
 }
 
 template <int FORM>
-void *kernel_for(int lanes) {
+void *kernel_for(int lanes, int plain) {
   switch (lanes) {
     case 8:
-      if (group_kind() == 2) return (void *)k_epoch_group_comb<FORM, 8, kCombT, kCombS>;
-      return group_kind() == 1 ? (void *)k_epoch_group_pipe<FORM, 8, kGrpE8, 4> : (void *)k_epoch_group<FORM, 8, kGrpE8>;
+      if (!plain && group_kind() == 2) return (void *)k_epoch_group_comb<FORM, 8, kCombT, kCombS>;
+      return (!plain && group_kind() == 1) ? (void *)k_epoch_group_pipe<FORM, 8, kGrpE8, 4> : (void *)k_epoch_group<FORM, 8, kGrpE8>;
     case 16:
       return group_kind() == 1 ? (void *)k_epoch_group_pipe<FORM, 16, 4, 4> : (void *)k_epoch_group<FORM, 16, 4>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
@@ -794,10 +794,15 @@ cudaEvent_t get_event(scd_ctx *c) {
 // Grid/block for a bin (used by build_schedule): persistent, sized to the SM count times the
 // kernel's residency, capped by max_inflight coordinates in flight.
 void bin_launch_shape(scd_ctx *c, Bin &b) {
-  void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
+  // A cap below a kernel's minimum batch must still be honoured (staleness): the
+  // combining kernel runs kCombT/8 coordinates per CTA, the 8-lane kernel >= 4 per warp, so small
+  // caps fall back to the plain 8-lane kernel, and caps below 4 to one warp per coordinate.
+  if (b.lanes == 8 && b.cap > 0 && b.cap < kCombT / 8) b.plain = 1;
+  if (b.lanes == 8 && b.cap > 0 && b.cap < 4) b.lanes = 32;
+  void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
   const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
-  const bool comb = (b.lanes == 8 && group_kind() == 2);  // fixed CTA size (kernel template)
+  const bool comb = (b.lanes == 8 && !b.plain && group_kind() == 2);  // fixed CTA size (kernel template)
   int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : kCtaT));
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
   if (group && !comb && b.cap > 0 && b.cap * b.lanes < block) {
@@ -876,7 +881,7 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch) {
         e1 = get_event(c);
         cudaEventRecord(e0, s);
       }
-      void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
+      void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
       void *args[] = {&a, &ba};
       SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)(grid * unit)), dim3(b.block), args, 0, s));
       ++c->launches;
@@ -922,7 +927,7 @@ scd_status tune_shared_layout(scd_ctx *c) {
     ba.hi = probe;
     ba.perm = make_perm(c->opt.seed ^ 0x5052424Full, 0xFFFFFFFEu, b.stream_id, b.count);
     ba.dry = 1;
-    void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes) : kernel_for<SCD_DUAL>(b.lanes);
+    void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
     float ms_min = 1e30f;
     for (int rep = 0; rep < 2; ++rep) {
       ba.counter = c->counters + rep;
