@@ -110,6 +110,14 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
  * context stream; returns without synchronising.                                               */
 scd_status scd_epoch(scd_ctx *c, uint32_t epoch);
 
+/* Part `part` (0 <= part < nparts <= 1024) of epoch `epoch`: the coordinates at positions
+ * [n·part/nparts, n·(part+1)/nparts) of every bin's permutation (the deterministic mode: of the
+ * epoch permutation).  Calling parts 0..nparts-1 in order updates every coordinate exactly once
+ * (in the deterministic mode it is exactly scd_epoch's sequence of updates); calling
+ * scd_aggregate between parts gives sub-epoch aggregation rounds — "communicate shared vector
+ * updates more frequently".  Enqueued only, like scd_epoch.            */
+scd_status scd_epoch_part(scd_ctx *c, uint32_t epoch, int32_t part, int32_t nparts);
+
 /* Primal and dual objectives, fp64, computed from scratch (the shared vector is NOT trusted).
  *   primal form: *primal = P(β), *dual = D((y - Aβ)/N)      (Eq. 6 map)
  *   dual form  : *primal = P(Aᵀα/λ), *dual = D(α)            (Eq. 5 map)

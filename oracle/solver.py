@@ -114,7 +114,7 @@ def solve(pr: Problem, form: str, epochs: int, seed: int, first_epoch: int = 1, 
 
 
 def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed: int, seed_part: int,
-                    first_epoch: int = 1, record: bool = True):
+                    first_epoch: int = 1, record: bool = True, parts: int = 1):
     """Distributed SCD, Alg. 3 (mode 'average', γ = 1/K) / 'add' (γ = 1) /
     Alg. 4 (mode 'optimal', γ from Eq. 7 corrected), simulated with K logical workers.
 
@@ -123,6 +123,9 @@ def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed
     local_ids[permutation(seed + k, t, |local_ids|)].  λN uses the global N (c14).  Every worker
     starts the round from the broadcast shared vector and its base model (c6); the aggregation
     scalars are taken at the base point (c5).
+    parts > 1: sub-epoch rounds ("communicate shared vector updates more frequently"):
+    round r runs part p = r mod parts of epoch t = first_epoch + r div parts, i.e. the positions
+    [len·p/parts, len·(p+1)/parts) of each worker's epoch order, then aggregates.
     Returns (model, shared, history) with history[i] = dict(epoch, gamma, P, D, gap)."""
     A = pr.A() if record else None
     n_coord = pr.M if form == "primal" else pr.N
@@ -138,13 +141,15 @@ def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed
         s0 = np.zeros(pr.M)      # w̄ = Aᵀα
         nrm = pr.row_norms()
     hist = []
-    for t in range(first_epoch, first_epoch + rounds):
+    for r in range(rounds):
+        t, p = first_epoch + r // parts, r % parts
         dx = np.zeros_like(x0)
         ds = np.zeros_like(s0)
         for k in range(K):
             xk = x0.copy()
             sk = s0.copy()
-            order = local[k][permutation(seed + k, t, len(local[k]))]
+            nk = len(local[k])
+            order = local[k][permutation(seed + k, t, nk)[nk * p // parts: nk * (p + 1) // parts]]
             if form == "primal":
                 primal_epoch(pr, xk, sk, order, nrm)
             else:

@@ -238,9 +238,16 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
   return SCD_OK;
 }
 
+scd_status scd_epoch_part(scd_ctx *c, uint32_t epoch, int32_t part, int32_t nparts) {
+  CK_CTX(c);
+  if (nparts < 1 || part < 0 || part >= nparts || nparts > 1024)
+    return fail(c, SCD_E_INVALID_ARG, "need 0 <= part < nparts <= 1024");
+  return run_epoch(c, epoch, part, nparts);
+}
+
 scd_status scd_epoch(scd_ctx *c, uint32_t epoch) {
   CK_CTX(c);
-  scd_status st = run_epoch(c, epoch);
+  scd_status st = run_epoch(c, epoch, 0, 1);
   if (st != SCD_OK) return st;
   ++c->epochs_done;
   if (c->opt.recompute_every > 0 && (c->epochs_done % (uint32_t)c->opt.recompute_every) == 0) {

@@ -177,7 +177,7 @@ scd_status transpose_device(const int64_t *ptr, const int32_t *idx, const float 
                             int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, cudaStream_t s, std::string &err);
 
 // epoch.cu -------------------------------------------------------------------------------------
-scd_status run_epoch(scd_ctx *c, uint32_t epoch);
+scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts);
 scd_status profile_collect(scd_ctx *c);
 scd_status tune_shared_layout(scd_ctx *c);
 void bin_launch_shape(scd_ctx *c, Bin &b);

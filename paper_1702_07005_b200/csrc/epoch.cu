@@ -592,11 +592,11 @@ __global__ void __launch_bounds__(T) k_epoch_group_comb(EpochArgs a, BinArgs b) 
 // unique indices within a coordinate, so there is no race.
 constexpr int kDbgT = 256;
 template <int FORM>
-__global__ void __launch_bounds__(kDbgT) k_epoch_debug(EpochArgs a, Perm perm, int64_t n) {
+__global__ void __launch_bounds__(kDbgT) k_epoch_debug(EpochArgs a, Perm perm, int64_t j0, int64_t j1) {
   __shared__ float s_red[kDbgT / 32];
   __shared__ float s_delta;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int64_t j = 0; j < n; ++j) {
+  for (int64_t j = j0; j < j1; ++j) {
     const int64_t c = (int64_t)perm_apply(perm, (uint64_t)j);
     const int64_t beg = a.ptr[c], end = a.ptr[c + 1];
     float acc = 0.f;
@@ -828,15 +828,18 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   b.block = block;
 }
 
-scd_status run_epoch(scd_ctx *c, uint32_t epoch) {
+// Part `part` of `nparts` of epoch `epoch`: permutation positions [n·part/nparts, n·(part+1)/nparts)
+// (sub-epoch aggregation rounds; nparts = 1 is a whole epoch).
+scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
   EpochArgs a = make_args(c);
   cudaStream_t s = c->stream;
   if (c->opt.deterministic) {
     Perm p = make_perm(c->opt.seed, epoch, 0u, c->n_coord);
+    const int64_t j0 = c->n_coord * part / nparts, j1 = c->n_coord * (part + 1) / nparts;
     if (c->form == SCD_PRIMAL)
-      k_epoch_debug<SCD_PRIMAL><<<1, kDbgT, 0, s>>>(a, p, c->n_coord);
+      k_epoch_debug<SCD_PRIMAL><<<1, kDbgT, 0, s>>>(a, p, j0, j1);
     else
-      k_epoch_debug<SCD_DUAL><<<1, kDbgT, 0, s>>>(a, p, c->n_coord);
+      k_epoch_debug<SCD_DUAL><<<1, kDbgT, 0, s>>>(a, p, j0, j1);
     SCD_CKL(c, "k_epoch_debug launch");
     ++c->launches;
     c->empty_dirty = false;
@@ -857,14 +860,16 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch) {
   // that, at the granularity of a slice, the epoch order stays a random mix of all coordinates
   // (a bin-by-bin order converges much more slowly, DESIGN.md §6 / reading c24).
   const int S = c->n_slices;
+  const int64_t Q = (int64_t)S * nparts;  // slices of the whole epoch; this part runs S of them
   SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins * S, s));
   for (int sl = 0; sl < S; ++sl) {
+    const int64_t q = (int64_t)part * S + sl;
     for (int i = 0; i < c->n_bins; ++i) {
       Bin &b = c->bins[i];
       BinArgs ba;
       ba.list = b.list;
-      ba.lo = b.count * sl / S;
-      ba.hi = b.count * (sl + 1) / S;
+      ba.lo = b.count * q / Q;
+      ba.hi = b.count * (q + 1) / Q;
       if (ba.hi <= ba.lo) continue;
       ba.counter = c->counters + sl * kMaxBins + i;
       ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.count);

@@ -50,7 +50,7 @@ class Info(C.Structure):
 
 
 _lib = None
-EXPORTS = ("scd_default_options", "scd_create", "scd_epoch", "scd_objective", "scd_duality_gap", "scd_aggregate",
+EXPORTS = ("scd_default_options", "scd_create", "scd_epoch", "scd_epoch_part", "scd_objective", "scd_duality_gap", "scd_aggregate",
            "scd_aggregate_group", "scd_get_model", "scd_get_shared", "scd_set_model", "scd_recompute_shared",
            "scd_get_stream", "scd_get_info", "scd_profile_read", "scd_last_error", "scd_last_global_error",
            "scd_status_string", "scd_destroy", "scd_permutation", "scd_partition", "scd_transpose",
@@ -69,6 +69,7 @@ def lib():
             "scd_default_options": (None, [C.POINTER(Options)]),
             "scd_create": (C.c_int, [C.POINTER(Matrix), P, C.c_int, D, C.c_int, C.POINTER(Options), C.POINTER(V)]),
             "scd_epoch": (C.c_int, [V, U32]),
+            "scd_epoch_part": (C.c_int, [V, U32, I32, I32]),
             "scd_objective": (C.c_int, [V, C.POINTER(D), C.POINTER(D)]),
             "scd_duality_gap": (C.c_int, [V, C.POINTER(D)]),
             "scd_aggregate": (C.c_int, [V, C.c_int, C.POINTER(D)]),
@@ -172,6 +173,10 @@ class Solver:
     # --- hot path -----------------------------------------------------------------------------
     def epoch(self, t: int):
         _check(lib().scd_epoch(self._h, t & 0xFFFFFFFF), self._h)
+
+    def epoch_part(self, t: int, part: int, nparts: int):
+        """Part `part` of `nparts` of epoch t (sub-epoch aggregation rounds)."""
+        _check(lib().scd_epoch_part(self._h, t & 0xFFFFFFFF, part, nparts), self._h)
 
     def objective(self) -> tuple[float, float]:
         P, D = C.c_double(), C.c_double()

@@ -347,3 +347,24 @@ def test_implicit_values_equal_explicit_ones(form):
         c.epoch(t)
     xs, _, hist = solver.solve(pr, form, 5, seed=2)
     assert c.duality_gap() <= max(10 * hist[-1]["gap"], 1e-7)
+
+
+@pytest.mark.parametrize("form", ["primal", "dual"])
+def test_sub_epoch_aggregation_matches_oracle(form):
+    """scd_epoch_part + scd_aggregate_group (sub-epoch rounds) vs the oracle simulator."""
+    d = synth.gen_host(synth.CONFIGS["C2"].with_rows(1200))
+    pr = solver.Problem.from_csr(d)
+    K, seed, sp_, parts, rounds = 3, 21, 5, 3, 6
+    xo, so, hist = solver.run_distributed(pr, form, K, "optimal", rounds, seed=seed, seed_part=sp_, parts=parts)
+    solvers = [scd.Solver(p, i, v, nr, nc, y, pr.lam, form, seed=seed + k, deterministic=True, n_global=pr.N)
+               for k, (p, i, v, nr, nc, y) in enumerate(_shards(d, pr, form, K, sp_))]
+    for r in range(rounds):
+        for s in solvers:
+            s.epoch_part(1 + r // parts, r % parts, parts)
+        g = scd.aggregate_group(solvers, "optimal")
+        assert g == pytest.approx(hist[r]["gamma"], rel=1e-4, abs=1e-7)
+    owner = oracle.partition(sp_, pr.M if form == "primal" else pr.N, K)
+    x = np.zeros(len(owner))
+    for k, s in enumerate(solvers):
+        x[owner == k] = s.get_model()
+    assert _rel(x, xo) <= 1e-4

@@ -401,3 +401,15 @@ def test_transpose_examples_and_involution():
     # [[1,0],[0,2]] cols -> (1, 4); [[1,2],[3,4]] rows -> (5, 25)
     assert oracle.sq_norms([0, 1, 2], [1.0, 2.0]).tolist() == [1.0, 4.0]
     assert oracle.sq_norms([0, 2, 4], [1.0, 2.0, 3.0, 4.0]).tolist() == [5.0, 25.0]
+
+
+def test_sub_epoch_rounds_cover_each_coordinate_once_and_converge_faster():
+    """Sub-epoch aggregation: with K = 1 and γ = 1 the parts of an epoch compose to the
+    whole epoch exactly; with K = 8 more frequent rounds need no more epochs than one round per epoch."""
+    pr = _rand_prob(300, 120, 0.1, 91, 1e-3)
+    x1, s1, _ = solver.run_distributed(pr, "primal", 1, "add", 3, seed=4, seed_part=1)
+    x4, s4, _ = solver.run_distributed(pr, "primal", 1, "add", 12, seed=4, seed_part=1, parts=4)
+    np.testing.assert_allclose(x4, x1, rtol=1e-12, atol=1e-15)
+    _, _, h1 = solver.run_distributed(pr, "primal", 8, "average", 10, seed=4, seed_part=1)
+    _, _, h4 = solver.run_distributed(pr, "primal", 8, "average", 40, seed=4, seed_part=1, parts=4)
+    assert h4[-1]["gap"] <= h1[-1]["gap"]
