@@ -1,0 +1,64 @@
+"""Small end-to-end exercise of every kernel family for compute-sanitizer (memcheck / racecheck):
+deterministic and asynchronous epochs (CTA, sub-warp, combining, cluster bins), empty rows/cols,
+implicit values, gap/objective, aggregation (group and 1-rank NCCL), transpose, permutation."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_1702_07005_b200 as scd  # noqa: E402
+
+
+def run(d, form, **kw):
+    p, i, v = d["ptr"], d["idx"], d["val"]
+    if form == "primal":
+        p, i, v = scd.transpose(p, i, v, d["n_rows"], d["n_cols"], "csr")
+    s = scd.Solver(p, i, v, d["n_rows"], d["n_cols"], d["y"], d["lam"], form, seed=3, **kw)
+    for t in (1, 2):
+        s.epoch(t)
+    s.epoch_part(3, 0, 2)
+    s.epoch_part(3, 1, 2)
+    g = s.duality_gap()
+    P, D = s.objective()
+    s.aggregate("optimal")
+    s.get_shared()
+    s.close()
+    return g, P, D
+
+
+# mixed lengths: short (group/comb), medium (warp), long (CTA) and very long (cluster) coordinates
+rng = np.random.default_rng(0)
+n_rows, n_cols = 6000, 3000
+lens = np.concatenate([rng.integers(1, 60, 2900), rng.integers(100, 900, 80), rng.integers(2000, 5900, 15),
+                       np.full(5, 5990)])
+rows = []
+for c, L in enumerate(lens):
+    rows.append(np.sort(rng.choice(n_rows, size=min(L, n_rows), replace=False)))
+ptr = np.zeros(n_cols + 1, np.int64)
+ptr[1:] = np.cumsum([len(r) for r in rows])
+cidx = np.concatenate(rows).astype(np.int32)
+cval = rng.random(len(cidx)).astype(np.float32)
+# this is CSC (columns); make the CSR view for the dual
+rp, ri, rv = scd.transpose(ptr, cidx, cval, n_rows, n_cols, "csc")
+d = dict(ptr=rp, idx=ri, val=rv, y=np.sign(rng.standard_normal(n_rows)).astype(np.float32), n_rows=n_rows,
+         n_cols=n_cols, lam=1e-2)
+for form in ("dual", "primal"):
+    for kw in (dict(deterministic=True), dict(), dict(max_inflight=3)):
+        print(form, kw, run(d, form, **kw), flush=True)
+c5 = synth.gen_host(synth.c5_scaled(4000, 1e-3))
+c5["val"] = None
+print("implicit", run(c5, "dual"), flush=True)
+e = synth.random_sparse(300, 200, 0.05, 3, empty_rows=7, empty_cols=9)
+print("empty", run(e, "dual"), run(e, "primal"), flush=True)
+uid = scd.nccl_unique_id()
+comm = scd.nccl_comm_init(uid, 1, 0)
+print("nccl", run(e, "dual", nccl_comm=comm), flush=True)
+scd.nccl_comm_destroy(comm)
+a = [scd.Solver(e["ptr"], e["idx"], e["val"], 300, 200, e["y"], 0.01, "dual", seed=k) for k in range(2)]
+for s in a:
+    s.epoch(1)
+print("group", scd.aggregate_group(a, "optimal"))
+assert np.array_equal(np.sort(scd.permutation(1, 2, 1000)), np.arange(1000))
+print("sanitize_small done")
