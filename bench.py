@@ -268,6 +268,24 @@ def main():
             traffic = None
     kernel_share = (ms_b / (el_ms if world == 1 else el_ms)) if cnt_b else None
 
+    # access-pattern ceiling on this box: the same gathers + REDs over the same matrix with no
+    # algorithmic dependency (tools/pattern_bench.cu), against a scratch vector
+    pattern = None
+    pso = os.path.join(ROOT, "tools", "libpattern.so")
+    if os.path.exists(pso):
+        import ctypes as C
+
+        pl = C.CDLL(pso)
+        pl.pattern_run.restype = C.c_float
+        pl.pattern_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        scratch = torch.zeros(cfg.n_cols + 1024, device="cuda")
+        sink = torch.zeros(1, device="cuda")
+        pms = min(pl.pattern_run(3, d["idx"].data_ptr(), d["val"].data_ptr(), nnz, scratch.data_ptr(),
+                                 sink.data_ptr()) for _ in range(2))
+        pattern = {"ms": pms, "entries_per_s": nnz / (pms / 1e3), "epoch_over_pattern": ms_step / pms,
+                   "what": "gather + red.add of sv[idx] for every stored entry, storage order, no dependencies"}
+        del scratch
+
     # time to duality gap 1e-4 from a fresh start (epoch + aggregation time only, gap off the clock)
     ttg = None
     if not args.no_ttg:
@@ -349,6 +367,7 @@ def main():
                          "kernel_ms_avg": ms_b / cnt_b if cnt_b else None, "kernel_share_of_step": kernel_share,
                          "bytes_per_launch": bytes_launch, "peak_source": peak_src,
                          "byte_model": "16 B/nnz (idx+val+gather+atomic) + 32 B/coordinate"},
+            "access_pattern_ceiling": pattern,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "setup_s": {"generate": t_gen, "create": t_create},

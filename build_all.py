@@ -90,11 +90,20 @@ def build_oracle(verbose=False, force=False):
     return out
 
 
+def build_tools(verbose=False, force=False):
+    """Measurement tools used by bench.py (the access-pattern ceiling kernel)."""
+    src = os.path.join(ROOT, "tools", "pattern_bench.cu")
+    out = os.path.join(ROOT, "tools", "libpattern.so")
+    if os.path.exists(src) and (force or _stale(out, [src])):
+        _run([nvcc(), *ARCH, "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", src, "-o", out], verbose)
+
+
 def build(verbose=False, force=False, product=True):
     build_oracle(verbose, force)
     build_synth(verbose, force)
     if product:
         build_product(verbose, force)
+        build_tools(verbose, force)
 
 
 if __name__ == "__main__":
