@@ -142,6 +142,10 @@ scd_status scd_aggregate(scd_ctx *c, scd_agg mode, double *gamma);
  * dual).  Used to test the distributed algorithm without a multi-GPU box.  Syncs.            */
 scd_status scd_aggregate_group(scd_ctx *const *ctxs, int32_t k, scd_agg mode, double *gamma);
 
+/* Objectives and duality gap (as scd_objective / scd_duality_gap) of the global model held by k
+ * logical workers on one device (the shards of scd_aggregate_group).  Any output may be NULL.  */
+scd_status scd_evaluate_group(scd_ctx *const *ctxs, int32_t k, double *primal, double *dual, double *gap);
+
 /* Copies β_k (primal, length n_cols) or α_k (dual, length n_rows) to host memory. Syncs. */
 scd_status scd_get_model(scd_ctx *c, float *host_out, int64_t len);
 /* Copies the shared vector w = Aβ (primal, length N) or w̄ = Aᵀα (dual, length M) to host.

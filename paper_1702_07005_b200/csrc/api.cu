@@ -294,6 +294,20 @@ scd_status scd_aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, doub
   return st;
 }
 
+scd_status scd_evaluate_group(scd_ctx *const *cs, int32_t k, double *primal, double *dual, double *gap) {
+  g_err.clear();
+  if (!cs || k < 1) return fail(nullptr, SCD_E_INVALID_ARG, "need k >= 1 contexts");
+  for (int i = 0; i < k; ++i) {
+    if (!cs[i]) return fail(nullptr, SCD_E_INVALID_ARG, "NULL context");
+    if (cs[i]->form != cs[0]->form || cs[i]->n_shared != cs[0]->n_shared || cs[i]->lam != cs[0]->lam ||
+        cs[i]->device != cs[0]->device || cs[i]->n_global != cs[0]->n_global || cs[i]->nccl)
+      return fail(nullptr, SCD_E_INVALID_ARG, "group contexts must share form, shared length, lambda, N, device; no comm");
+  }
+  scd_status st = evaluate_group(cs, k, primal, dual, gap);
+  if (st != SCD_OK) g_err = cs[0]->err;
+  return st;
+}
+
 scd_status scd_get_model(scd_ctx *c, float *host_out, int64_t len) {
   CK_CTX(c);
   if (!host_out || len != c->n_coord) return fail(c, SCD_E_INVALID_ARG, "model length mismatch");

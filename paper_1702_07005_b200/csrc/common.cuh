@@ -186,6 +186,7 @@ scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int3
 
 // evaluate.cu ----------------------------------------------------------------------------------
 scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap);
+scd_status evaluate_group(scd_ctx *const *cs, int32_t k, double *primal, double *dual, double *gap);
 scd_status rebuild_shared(scd_ctx *c);
 scd_status shared_to_w(scd_ctx *c, float *d_out);
 

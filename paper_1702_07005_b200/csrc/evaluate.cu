@@ -172,6 +172,53 @@ scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap) {
   return SCD_OK;
 }
 
+// The same evaluation for k logical workers on one device (scd_aggregate_group's setting): the
+// shard scatters are summed into ctx 0's fp64 vector (the all-reduce), per-shard partial sums go
+// into ctx 0's accumulators; replicated quantities are computed once.
+scd_status evaluate_group(scd_ctx *const *cs, int32_t k, double *primal, double *dual, double *gap) {
+  scd_ctx *c0 = cs[0];
+  for (int i = 0; i < k; ++i) SCD_CK(cs[i], cudaStreamSynchronize(cs[i]->stream));
+  cudaStream_t s = c0->stream;
+  SCD_CK(c0, cudaMemsetAsync(c0->vec64, 0, sizeof(double) * (size_t)c0->n_shared, s));
+  SCD_CK(c0, cudaMemsetAsync(c0->acc, 0, sizeof(double) * 8, s));
+  for (int i = 0; i < k; ++i) {
+    scd_ctx *c = cs[i];
+    k_scatter64<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->n_coord,
+                                                                        c0->vec64);
+    ++c->launches;
+  }
+  const double N = (double)c0->n_global, lam = c0->lam;
+  double h[8] = {0};
+  if (c0->form == SCD_PRIMAL) {
+    k_primal_rows<<<grid_for(c0->n_shared, kT, 148 * 8), kT, 0, s>>>(c0->y, c0->vec64, c0->n_shared, c0->acc);
+    for (int i = 0; i < k; ++i) {
+      scd_ctx *c = cs[i];
+      k_primal_cols<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c0->vec64,
+                                                                            c->n_coord, lam, N, c0->acc);
+    }
+  } else {
+    k_sumsq64<<<grid_for(c0->n_shared, kT, 148 * 8), kT, 0, s>>>(c0->vec64, c0->n_shared, c0->acc + 0);
+    for (int i = 0; i < k; ++i) {
+      scd_ctx *c = cs[i];
+      k_dual_rows<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->y,
+                                                                          c0->vec64, c->n_coord, lam, N, c0->acc);
+    }
+  }
+  SCD_CKL(c0, "evaluate_group kernels");
+  SCD_CK(c0, cudaMemcpyAsync(h, c0->acc, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
+  SCD_CK(c0, cudaStreamSynchronize(s));
+  if (c0->form == SCD_PRIMAL) {
+    if (primal) *primal = h[0] / (2.0 * N) + 0.5 * lam * h[3];
+    if (dual) *dual = -0.5 * N * (h[0] / (N * N)) - (h[4] / (N * N)) / (2.0 * lam) + h[1] / N;
+    if (gap) *gap = h[2] / (2.0 * lam);
+  } else {
+    if (primal) *primal = h[1] / (2.0 * N) + h[0] / (2.0 * lam);
+    if (dual) *dual = -0.5 * N * h[3] - h[0] / (2.0 * lam) + h[4];
+    if (gap) *gap = h[2] / (2.0 * N);
+  }
+  return SCD_OK;
+}
+
 // Shared vector from the model (fp64 accumulate, one rounding to fp32); resets the base point.
 scd_status rebuild_shared(scd_ctx *c) {
   cudaStream_t s = c->stream;

@@ -51,7 +51,7 @@ class Info(C.Structure):
 
 _lib = None
 EXPORTS = ("scd_default_options", "scd_create", "scd_epoch", "scd_epoch_part", "scd_objective", "scd_duality_gap", "scd_aggregate",
-           "scd_aggregate_group", "scd_get_model", "scd_get_shared", "scd_set_model", "scd_recompute_shared",
+           "scd_aggregate_group", "scd_evaluate_group", "scd_get_model", "scd_get_shared", "scd_set_model", "scd_recompute_shared",
            "scd_get_stream", "scd_get_info", "scd_profile_read", "scd_last_error", "scd_last_global_error",
            "scd_status_string", "scd_destroy", "scd_permutation", "scd_partition", "scd_transpose",
            "scd_nccl_unique_id", "scd_nccl_comm_init", "scd_nccl_comm_destroy")
@@ -74,6 +74,7 @@ def lib():
             "scd_duality_gap": (C.c_int, [V, C.POINTER(D)]),
             "scd_aggregate": (C.c_int, [V, C.c_int, C.POINTER(D)]),
             "scd_aggregate_group": (C.c_int, [P, I32, C.c_int, C.POINTER(D)]),
+            "scd_evaluate_group": (C.c_int, [P, I32, C.POINTER(D), C.POINTER(D), C.POINTER(D)]),
             "scd_get_model": (C.c_int, [V, P, I64]),
             "scd_get_shared": (C.c_int, [V, P, I64]),
             "scd_set_model": (C.c_int, [V, P, I64]),
@@ -259,6 +260,14 @@ def aggregate_group(solvers, mode: str = "optimal") -> float:
     g = C.c_double()
     _check(lib().scd_aggregate_group(arr, len(solvers), AGG[mode], C.byref(g)))
     return g.value
+
+
+def evaluate_group(solvers) -> tuple[float, float, float]:
+    """(P, D, gap) of the global model of logical workers on one device."""
+    arr = (C.c_void_p * len(solvers))(*[s._h.value for s in solvers])
+    P, D, g = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().scd_evaluate_group(arr, len(solvers), C.byref(P), C.byref(D), C.byref(g)))
+    return P.value, D.value, g.value
 
 
 def permutation(seed: int, epoch: int, n: int, stream: int = 0) -> np.ndarray:
