@@ -207,9 +207,8 @@ def main():
         t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
         dist.broadcast(t, 0)
         comm = scd.nccl_comm_init(bytes(t.cpu().tolist()), world, rank)
-    # The library creates its own stream (measured: epochs enqueued on a torch-pool stream ran 24%
-    # slower on the same box); torch only wraps it to record the timing events.
-    kw = dict(seed=3, n_global=rows * world, rank=rank, world=world, nccl_comm=comm, max_inflight=args.max_inflight)
+    # The library creates its own stream; torch only wraps it to record the timing events.
+    kw = dict(seed=3 + rank, n_global=rows * world, rank=rank, world=world, nccl_comm=comm, max_inflight=args.max_inflight)
     t_create = time.perf_counter()
     s = scd.Solver(d["ptr"], d["idx"], d["val"], rows, cfg.n_cols, d["y"], cfg.lam, "dual", profile=True, **kw)
     t_create = time.perf_counter() - t_create
