@@ -258,11 +258,17 @@ def main():
     # one launch processes one of the n_slices slices of the bin
     bytes_launch = (BYTES_PER_NNZ * bins[b_i]["nnz"] + BYTES_PER_COORD * bins[b_i]["count"]) / info["n_slices"]
     achieved = bytes_launch / (ms_b / cnt_b / 1e3) / 1e9 if cnt_b else None
+    bb = bins[b_i]
+    kname = ("k_epoch_split" if bb.get("split") else "k_epoch_cta_head" if bb.get("head") else "k_epoch_cta") \
+        if bb["lanes"] >= 64 else "k_epoch_group"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            # only a capture of the same kernel counts (names: "...k_epoch_cta_head<1, 256, 16>...")
+            if (kname + "<") in tj.get("kernel", ""):
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     kernel_share = (ms_b / (el_ms if world == 1 else el_ms)) if cnt_b else None
@@ -361,8 +367,9 @@ def main():
             "hbm_gbs": (BYTES_PER_NNZ * total_nnz + BYTES_PER_COORD * rows * world) / (ms_step / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": f"k_epoch_{'cta' if bins[b_i]['lanes'] >= 64 else 'group'} (bin {b_i}, "
-                                   f"{bins[b_i]['lanes']} lanes/coord)",
+                         "kernel": f"{kname} (bin {b_i}, {bb['lanes']} lanes/coord"
+                                   + (f", head {bb['head']} floats combined, flush every {bb['flush']}" if bb.get("head") else "")
+                                   + ")",
                          "kernel_ms_avg": ms_b / cnt_b if cnt_b else None, "kernel_share_of_step": kernel_share,
                          "bytes_per_launch": bytes_launch, "peak_source": peak_src,
                          "byte_model": "16 B/nnz (idx+val+gather+atomic) + 32 B/coordinate"},

@@ -181,6 +181,14 @@ typedef struct {
   int64_t sv_offset_bytes;/* placement of the shared vector chosen at create */
   float probe_best_ms;    /* placement probe: fastest / slowest candidate (0 if not probed) */
   float probe_worst_ms;
+  int32_t bin_head[4];    /* per bin: > 0 = the CTA kernel combines updates of sv[0, bin_head) in shared
+                             memory (head-combining kernel); 0 = plain */
+  int32_t bin_flush[4];   /* per bin: coordinates per CTA between flushes of the combined head */
+  int32_t bin_split[4];   /* per bin: 1 = die-split kernel (each coordinate split over the two dies) */
+  int32_t die_split;      /* 1 = the two-die placement is active */
+  int32_t n_die_sm[2];    /* SMs found on each die by the create-time probe */
+  float die_lat[2];       /* probe: near / far atomic round-trip latency (SM cycles) */
+  int64_t split_nnz0;     /* die split: stored entries whose shared-vector element is homed on die 0 */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

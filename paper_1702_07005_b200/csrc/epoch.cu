@@ -260,6 +260,261 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
 }
 
 // ----------------------------------------------------------------------------------------------
+// Head-combining CTA kernel (dense head of a frequency-ranked shared vector, webspam-shaped dual).
+// The L2 charges a reduction per 32-byte SECTOR, whatever number of fp32 elements of the sector it
+// carries, and a line that every coordinate updates serialises in its slice (tools/red_bench.cu,
+// profiles/red_bench_r1.txt).  The head [0, H) of w̄ is such a region: its entries are carried by
+// most rows.  So each CTA keeps its own pending updates of the head in shared memory (s_acc[H])
+// and flushes them every `flush` coordinates with one 16-byte red.global.add.v4.f32 per touched float4 — one L2 reduction per sector per `flush` rows instead of one per row.
+// One coordinate at a time per CTA and unique indices within a coordinate make the shared-memory
+// accumulation a plain read-modify-write (sm_100 has no native fp32 shared atomic add).
+// The CTA reads the head as L2 value + its own pending value, so a CTA always sees its own
+// updates; other CTAs' pending head updates are the extra staleness, at most (CTAs)·flush
+// coordinates, which build_schedule keeps under the bin's cap.  Tail entries
+// (id >= H) are gathered and reduced in L2 exactly as in k_epoch_cta.
+__device__ __forceinline__ void red_add_v4(float *p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+template <int T>
+__device__ __forceinline__ void head_flush(float *sv, float *s_acc, int H, int dry) {
+  float4 *a4 = reinterpret_cast<float4 *>(s_acc);
+  for (int i = threadIdx.x; i < H / 4; i += T) {
+    const float4 v = a4[i];
+    if (dry || v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f) {
+      red_add_v4(sv + 4 * i, v);
+      a4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+template <int FORM, int T, int E>
+__global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
+  constexpr int NW = T / 32;
+  extern __shared__ float4 s_dyn[];
+  float *s_acc = reinterpret_cast<float *>(s_dyn);
+  __shared__ float s_red[NW];
+  __shared__ float s_delta;
+  __shared__ unsigned int s_ticket;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < H; i += T) s_acc[i] = 0.f;
+  int since = 0;
+  for (;;) {
+    if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
+    __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
+    const int64_t t = b.lo + (int64_t)s_ticket;
+    if (t >= b.hi) break;
+    const int64_t c = bin_coord(b, t);
+    const int64_t beg = __ldg(a.ptr + c), end = __ldg(a.ptr + c + 1);
+    int32_t id[E];
+    float v[E];
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = beg + (int64_t)e * T + tid;
+      if (k < end) {
+        id[e] = __ldcs(a.idx + k);
+        v[e] = val_cs(a.val, k);
+      } else {
+        id[e] = -1;
+        v[e] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (id[e] >= 0) {
+        float w = ld_sv(a.sv + id[e]);
+        if (id[e] < H) w += s_acc[id[e]];
+        acc = fmaf(w, v[e], acc);
+      }
+    for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
+#pragma unroll 4
+      for (int e = 0; e < E; ++e) {
+        const int64_t k = base + (int64_t)e * T + tid;
+        if (k < end) {
+          const int32_t j = __ldcg(a.idx + k);
+          float w = ld_sv(a.sv + j);
+          if (j < H) w += s_acc[j];
+          acc = fmaf(w, val_cg(a.val, k), acc);
+        }
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+      float s = lane < NW ? s_red[lane] : 0.f;
+      s = warp_sum(s);
+      if (lane == 0) {
+        const float xc = a.x[c];
+        const float d = coord_delta<FORM>(s, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f,
+                                          a.lam, a.lamN);
+        if (!b.dry) a.x[c] = xc + d;  // single writer per epoch (c10)
+        s_delta = b.dry ? 0.f : d;
+      }
+    }
+    __syncthreads();
+    const float d = scatter_scale<FORM>(s_delta);
+    if (d != 0.f || b.dry) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (id[e] >= 0) {
+          if (id[e] < H)
+            s_acc[id[e]] += v[e] * d;  // ids unique within a coordinate: no race
+          else
+            red_add(a.sv + id[e], v[e] * d);
+        }
+      for (int64_t k0 = beg + (int64_t)T * E + tid; k0 < end; k0 += (int64_t)T * 4) {
+        int32_t jj[4];
+        float vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t kk = k0 + (int64_t)u * T;
+          jj[u] = kk < end ? __ldcg(a.idx + kk) : -1;
+          vv[u] = kk < end ? val_cg(a.val, kk) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (jj[u] >= 0) {
+            if (jj[u] < H)
+              s_acc[jj[u]] += vv[u] * d;
+            else
+              red_add(a.sv + jj[u], vv[u] * d);
+          }
+      }
+    }
+    if (++since == flush) {
+      since = 0;
+      __syncthreads();
+      head_flush<T>(a.sv, s_acc, H, b.dry);
+    }
+  }
+  head_flush<T>(a.sv, s_acc, H, b.dry);  // after the exit barrier: every smem atomic has landed
+}
+
+// ----------------------------------------------------------------------------------------------
+// Die-split CTA kernel (die.cu).  Every coordinate is processed by two CTAs, one on
+// each die, each over the part of the coordinate's entries whose shared-vector element is homed in
+// its own die's L2 (entries reordered at create: [ptr[c], mid[c]) die 0, [mid[c], ptr[c+1]) die 1).
+// CTAs of die d take tickets from die d's counter, so both dies walk the same permutation.  The two
+// partial dot products meet in a global slot (release/acquire, tagged with the launch); both CTAs
+// form dp = p0 + p1 in that order, hence the same Δ; the die-0 CTA is the single writer of x[c]
+// (c10) and each CTA scatters its own part.  The die-1 CTA reads x[c] before publishing its
+// partial, i.e. before die 0 can write it.  A CTA publishes before it waits, so the lowest
+// outstanding ticket always completes: no deadlock while every CTA is resident (grid <= occupancy).
+struct SplitArgs {
+  const int64_t *mid;
+  const int32_t *idx;
+  const float *val;  // nullptr = implicit values
+  const uint8_t *sm_die;
+  float *slot_p;
+  unsigned *slot_tag;
+  unsigned *err;
+  unsigned *counter1;  // die 1's ticket counter (die 0 uses BinArgs::counter)
+  unsigned tag;
+  int nosync;          // diagnostic only: no partner exchange (wrong Δ), isolates the rendezvous cost
+};
+
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned smid_now() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+template <int FORM, int T, int E>
+__global__ void __launch_bounds__(T, 4) k_epoch_split(EpochArgs a, BinArgs b, SplitArgs s) {
+  constexpr int NW = T / 32;
+  __shared__ float s_red[NW];
+  __shared__ float s_delta;
+  __shared__ unsigned int s_ticket;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int die = s.sm_die[smid_now()];  // a CTA never migrates
+  unsigned *counter = die == 0 ? b.counter : s.counter1;
+  for (;;) {
+    if (tid == 0) s_ticket = atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t t = b.lo + (int64_t)s_ticket;
+    if (t >= b.hi) break;
+    const int64_t c = bin_coord(b, t);
+    const int64_t m = __ldg(s.mid + c);
+    const int64_t beg = die == 0 ? __ldg(a.ptr + c) : m;
+    const int64_t end = die == 0 ? m : __ldg(a.ptr + c + 1);
+    float xc = 0.f;
+    if (tid == 0) xc = a.x[c];  // before publishing (see above)
+    int32_t id[E];
+    float v[E];
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = beg + (int64_t)e * T + tid;
+      if (k < end) {
+        id[e] = __ldcs(s.idx + k);
+        v[e] = val_cs(s.val, k);
+      } else {
+        id[e] = -1;
+        v[e] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
+    for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
+#pragma unroll 4
+      for (int e = 0; e < E; ++e) {
+        const int64_t k = base + (int64_t)e * T + tid;
+        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(s.idx + k)), val_cg(s.val, k), acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+      float p = lane < NW ? s_red[lane] : 0.f;
+      p = warp_sum(p);
+      if (lane == 0) {
+        const int64_t q = 2 * t;
+        if (s.nosync) {
+          s.slot_p[q + 1 - die] = 0.f;
+          s.slot_tag[q + 1 - die] = s.tag;
+        }
+        s.slot_p[q + die] = p;
+        st_release(s.slot_tag + q + die, s.tag);
+        unsigned spins = 0;
+        while (ld_acquire(s.slot_tag + q + (1 - die)) != s.tag) {
+          if (++spins > (1u << 26)) {  // partner never arrived: flag it, do not hang
+            atomicExch(s.err, 1u);
+            break;
+          }
+        }
+        const float po = __ldcg(s.slot_p + q + (1 - die));
+        const float dp = die == 0 ? p + po : po + p;
+        const float d = coord_delta<FORM>(dp, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f,
+                                          a.lam, a.lamN);
+        if (die == 0 && !b.dry) a.x[c] = xc + d;  // single writer per epoch (c10)
+        s_delta = b.dry ? 0.f : d;
+      }
+    }
+    __syncthreads();
+    const float d = scatter_scale<FORM>(s_delta);
+    if (d != 0.f || b.dry) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
+      scatter_strided<4>(a.sv, s.idx, s.val, beg + (int64_t)T * E + tid, end, T, d);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
 template <int FORM, int G, int E>
 __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
   constexpr int CPW = 32 / G;  // coordinates per warp per ticket
@@ -764,6 +1019,16 @@ void *kernel_for(int lanes, int plain) {
   }
 }
 
+void *bin_kernel(const scd_ctx *c, const Bin &b) {
+  if (b.split && b.lanes == kLanesCta)
+    return c->form == SCD_PRIMAL ? (void *)k_epoch_split<SCD_PRIMAL, kCtaT, kCtaE>
+                                 : (void *)k_epoch_split<SCD_DUAL, kCtaT, kCtaE>;
+  if (b.head > 0 && b.lanes == kLanesCta)
+    return c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE>
+                                 : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE>;
+  return c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
+}
+
 EpochArgs make_args(scd_ctx *c) {
   EpochArgs a;
   a.ptr = c->ptr;
@@ -799,7 +1064,9 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   // caps fall back to the plain 8-lane kernel, and caps below 4 to one warp per coordinate.
   if (b.lanes == 8 && b.cap > 0 && b.cap < kCombT / 8) b.plain = 1;
   if (b.lanes == 8 && b.cap > 0 && b.cap < 4) b.lanes = 32;
-  void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
+  if (b.lanes != kLanesCta) b.head = b.split = 0;
+  if (b.split) b.head = 0;
+  void *fn = bin_kernel(c, b);
   const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
   const bool comb = (b.lanes == 8 && !b.plain && group_kind() == 2);  // fixed CTA size (kernel template)
@@ -809,14 +1076,16 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
     if (block < 32) block = 32;
   }
+  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head : 0;
+  if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
   if (occ < 1) occ = 1;
   const int per_launch_unit = clus ? kClusterCtas : 1;           // CTAs per coordinate slot
   const int coords_per_cta = group ? block / b.lanes : 1;
   int64_t slots = (int64_t)c->nsm * occ / per_launch_unit;        // resident coordinate slots
   if (clus && slots > (int64_t)c->nsm / kClusterCtas * occ) slots = (int64_t)c->nsm / kClusterCtas * occ;
-  int64_t units = group ? slots : slots;                          // CTAs (or clusters)
+  int64_t units = slots;                                          // CTAs (or clusters)
   if (b.cap > 0) {  // staleness cap
     int64_t u = (b.cap + coords_per_cta - 1) / coords_per_cta;
     if (u < units) units = u;
@@ -826,6 +1095,47 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   if (units < 1) units = 1;
   b.grid = (int)(units * per_launch_unit);
   b.block = block;
+  if (b.head > 0) {
+    // pending head updates of `flush` coordinates per CTA are in flight as far as other CTAs are
+    // concerned: grid * flush <= cap.  SCD_HEAD_FLUSH overrides (experiments only).
+    int64_t f = b.cap > 0 ? b.cap / b.grid : 16;
+    if (const char *e = getenv("SCD_HEAD_FLUSH")) f = atoi(e);
+    if (f > 64) f = 64;
+    if (f < 2) {  // no combining possible under the cap: plain CTA kernel
+      b.head = 0;
+      b.flush = 0;
+      bin_launch_shape(c, b);
+      return;
+    }
+    b.flush = (int)f;
+  }
+}
+
+// Launch one bin's kernel over the permutation positions [ba.lo, ba.hi) with `grid` CTAs.
+scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64_t grid, cudaStream_t s) {
+  void *fn = bin_kernel(c, b);
+  int H = b.head, F = b.flush;
+  void *args_head[] = {&a, &ba, &H, &F};
+  SplitArgs sa;
+  void *args_split[] = {&a, &ba, &sa};
+  void **args = args_head;
+  if (b.split) {
+    sa.mid = c->split_mid;
+    sa.idx = c->split_idx;
+    sa.val = c->split_val;
+    sa.sm_die = c->sm_die;
+    sa.slot_p = c->slot_p;
+    sa.slot_tag = c->slot_tag;
+    sa.err = c->split_err;
+    sa.counter1 = ba.counter + kMaxBins * kMaxSlices;    // die 1's counter: same (slice, bin), second half
+    if (++c->launch_tag == 0) ++c->launch_tag;                  // 0 = never written
+    sa.tag = c->launch_tag;
+    sa.nosync = c->split_nosync ? 1 : 0;
+    args = args_split;
+  }
+  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head : 0;
+  SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(b.block), args, smem, s));
+  return SCD_OK;
 }
 
 // Part `part` of `nparts` of epoch `epoch`: permutation positions [n·part/nparts, n·(part+1)/nparts)
@@ -862,6 +1172,8 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
   const int S = c->n_slices;
   const int64_t Q = (int64_t)S * nparts;  // slices of the whole epoch; this part runs S of them
   SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins * S, s));
+  if (c->die_split)
+    SCD_CK(c, cudaMemsetAsync(c->counters + kMaxBins * kMaxSlices, 0, sizeof(unsigned int) * kMaxBins * S, s));
   for (int sl = 0; sl < S; ++sl) {
     const int64_t q = (int64_t)part * S + sl;
     for (int i = 0; i < c->n_bins; ++i) {
@@ -886,9 +1198,8 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
         e1 = get_event(c);
         cudaEventRecord(e0, s);
       }
-      void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
-      void *args[] = {&a, &ba};
-      SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)(grid * unit)), dim3(b.block), args, 0, s));
+      scd_status st = launch_bin(c, b, a, ba, grid * unit, s);
+      if (st != SCD_OK) return st;
       ++c->launches;
       if (c->opt.profile) {
         cudaEventRecord(e1, s);
@@ -932,14 +1243,14 @@ scd_status tune_shared_layout(scd_ctx *c) {
     ba.hi = probe;
     ba.perm = make_perm(c->opt.seed ^ 0x5052424Full, 0xFFFFFFFEu, b.stream_id, b.count);
     ba.dry = 1;
-    void *fn = c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
     float ms_min = 1e30f;
     for (int rep = 0; rep < 2; ++rep) {
       ba.counter = c->counters + rep;
       SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2, s));
-      void *args[] = {&a, &ba};
+      SCD_CK(c, cudaMemsetAsync(c->counters + kMaxBins * kMaxSlices, 0, sizeof(unsigned int) * 2, s));
       SCD_CK(c, cudaEventRecord(e0, s));
-      SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)(b.grid * unit)), dim3(b.block), args, 0, s));
+      scd_status st = launch_bin(c, b, a, ba, (int64_t)b.grid * unit, s);
+      if (st != SCD_OK) return st;
       SCD_CK(c, cudaEventRecord(e1, s));
       SCD_CK(c, cudaEventSynchronize(e1));
       float ms = 0.f;

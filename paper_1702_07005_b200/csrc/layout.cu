@@ -105,7 +105,38 @@ double cap_fraction() {
   return f > 0 ? f : 0.5;
 }
 
+// number of stored entries with inner index < H (sizing the head-combining kernel)
+__global__ void __launch_bounds__(256) k_count_below(const int32_t *idx, int64_t n, int32_t H, unsigned long long *out) {
+  unsigned long long cnt = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    cnt += __ldcs(idx + i) < H;
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
+}
+
 }  // namespace
+
+// Head of the shared vector combined in shared memory by the CTA kernel (k_epoch_cta_head,
+// DESIGN.md §6): H = SCD_HEAD floats (default 8192, 0 = off), used when at least 10% of all
+// stored entries fall in [0, H) — the frequency-ranked head of a power-law feature distribution.
+static scd_status choose_head(scd_ctx *c, int *head) {
+  *head = 0;
+  int64_t H = 8192;
+  if (const char *e = getenv("SCD_HEAD")) H = atoll(e);
+  H = std::min<int64_t>(H, c->n_shared) / 4 * 4;
+  if (H < 256 || c->opt.deterministic || c->nnz == 0) return SCD_OK;
+  if (((uintptr_t)c->sv & 15) != 0) return SCD_OK;  // v4 flush needs 16-byte alignment
+  unsigned long long *d = nullptr, h = 0;
+  SCD_CK(c, cudaMallocAsync((void **)&d, sizeof(*d), c->stream));
+  SCD_CK(c, cudaMemsetAsync(d, 0, sizeof(*d), c->stream));
+  k_count_below<<<grid_for(c->nnz, 256, 148 * 8), 256, 0, c->stream>>>(c->idx, c->nnz, (int32_t)H, d);
+  SCD_CKL(c, "k_count_below");
+  SCD_CK(c, cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  SCD_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFreeAsync(d, c->stream);
+  if ((double)h >= 0.10 * (double)c->nnz) *head = (int)H;
+  return SCD_OK;
+}
 
 // Staleness bound for one bin of the asynchronous schedule.  With τ coordinates of
 // the bin in flight, a coordinate's update misses up to τ-1 concurrent updates.  Treating them as
@@ -190,6 +221,8 @@ scd_status build_schedule(scd_ctx *c) {
     SCD_CK(c, cudaMalloc((void **)&c->empty_list, sizeof(int32_t) * empty.size()));
     SCD_CK(c, cudaMemcpy(c->empty_list, empty.data(), sizeof(int32_t) * empty.size(), cudaMemcpyHostToDevice));
   }
+  int head = 0;
+  if (scd_status st = choose_head(c, &head); st != SCD_OK) return st;
   // launch order: longest coordinates first
   c->n_bins = 0;
   c->tau_star = 1e18;
@@ -211,6 +244,7 @@ scd_status build_schedule(scd_ctx *c) {
     if (B.tau < c->tau_star) c->tau_star = B.tau;
     double cap = cap_fraction() * B.tau;
     B.cap = c->opt.max_inflight > 0 ? (int64_t)c->opt.max_inflight : (int64_t)(cap < 1 ? 1 : (cap > 1e9 ? 1e9 : cap));
+    B.head = B.lanes == kLanesCta ? head : 0;
     bin_launch_shape(c, B);
     ++c->n_bins;
   }
@@ -220,7 +254,8 @@ scd_status build_schedule(scd_ctx *c) {
     int v = atoi(e);
     if (v >= 1 && v <= kMaxSlices) c->n_slices = v;
   }
-  SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * kMaxBins * kMaxSlices));
+  // two ticket counters per (slice, bin): the second feeds die 1 of the die-split kernel
+  SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices));
   return SCD_OK;
 }
 

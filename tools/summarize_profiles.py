@@ -1,6 +1,6 @@
 """Summaries for profiles/ (run here, on the CPU box, on files gpurun brought back).
 
-  python tools/summarize_profiles.py launches gpurun_out/launches.csv > profiles/launches_r1.md
+  python tools/summarize_profiles.py launches gpurun_out/launches.csv [last [skip_tail]] > profiles/launches_r1.md
   python tools/summarize_profiles.py ncu gpurun_out/prof.ncu-rep profiles/ncu_epoch_r1  [bytes_per_launch]
 
 `launches`: per-kernel launch count, total and mean device time, share of the listed time
@@ -18,15 +18,18 @@ import sys
 from collections import defaultdict
 
 
-def launches(path, last=0):
+def launches(path, last=0, skip=0):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     ki, vi, mi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
     agg = defaultdict(lambda: [0, 0.0])
     body = rows[1:]
+    if skip:
+        body = body[:-skip]
     if last:
         body = body[-last:]
-        print(f"Last {last} launches of the list (the timed region).\n")
+        print(f"Last {last} launches of the list" + (f" before the final {skip}" if skip else "") +
+              " (the timed region).\n")
     for r in body:
         if r[mi] != "gpu__time_duration.sum":
             continue
@@ -99,6 +102,6 @@ def ncu(rep, out_prefix, bytes_per_launch=None):
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        launches(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0)
+        launches(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0, int(sys.argv[4]) if len(sys.argv) > 4 else 0)
     else:
         ncu(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None)
