@@ -82,6 +82,11 @@ typedef struct {
   int32_t recompute_every;/* rebuild the shared vector from the model every k epochs; 0 = off */
   int32_t validate;       /* 1 = check the matrix invariants on the device at create (default 1) */
   int32_t profile;        /* 1 = time every kernel launch of scd_epoch with CUDA events (scd_profile_read) */
+  int32_t wild;           /* 1 = "wild" scatter: plain load + store instead of the atomic add, so concurrent
+                             updates of one shared-vector entry can be lost (PASSCoDe-Wild, P:164, P:254;
+                             SURVEY NEXT-4).  A measured comparison only: it converges to a point that
+                             violates the optimality conditions.  Uses the plain kernels (no head
+                             combining, no CTA combining).  0 = atomic (default, the paper's TPA-SCD). */
 } scd_options;
 
 typedef struct scd_ctx scd_ctx;

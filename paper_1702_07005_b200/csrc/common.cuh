@@ -147,6 +147,7 @@ struct scd_ctx {
   double tau_star = 0.0;   // smallest estimated staleness bound over the bins (layout.cu)
   // die-split epoch (die.cu): SM -> die map, each coordinate's entries reordered so
   // the ones whose shared-vector entry is homed in die 0's L2 come first
+  bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)
   bool die_split = false;
   uint8_t *sm_die = nullptr;          // device [kMaxSm]: die of each SM id
   int n_die_sm[2] = {0, 0};

@@ -135,7 +135,7 @@ scd_status setup_die_split(scd_ctx *c) {
   c->die_split = false;
   const char *e = getenv("SCD_DIE_SPLIT");
   if (!e || atoi(e) != 1) return die_off(c, 3);
-  if (c->opt.deterministic || c->nnz == 0) return die_off(c, 4);
+  if (c->opt.deterministic || c->opt.wild || c->nnz == 0) return die_off(c, 4);
   int64_t nsplit = 0, max_count = 0;
   for (int i = 0; i < c->n_bins; ++i)
     if (c->bins[i].lanes == kLanesCta && c->bins[i].grid >= c->nsm) {

@@ -63,10 +63,29 @@ __device__ __forceinline__ float scatter_scale(float d) { return FORM == SCD_PRI
 __device__ __forceinline__ float ld_sv(const float *p) { return __ldcg(p); }
 __device__ __forceinline__ void red_add(float *p, float v) { atomicAdd(p, v); }  // RED.E.ADD.F32
 
-// Atomic scatter of the entries k = k0 + j*stride (k < end) of a coordinate, U entries at a time
+// Scatter of U register-held entries (id < 0 = none).  Atomic: red.global.add.f32.  WILD (the
+// PASSCoDe-Wild comparison, options.wild): plain load + store, all loads issued before the stores, so
+// a concurrent update of the same entry between the two can be lost.
+template <bool WILD, int U>
+__device__ __forceinline__ void scatter_regs(float *sv, const int32_t *id, const float *v, float d) {
+  if (WILD) {
+    float o[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) o[u] = id[u] >= 0 ? __ldcg(sv + id[u]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (id[u] >= 0) __stcg(sv + id[u], o[u] + v[u] * d);
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (id[u] >= 0) red_add(sv + id[u], v[u] * d);
+  }
+}
+
+// Scatter of the entries k = k0 + j*stride (k < end) of a coordinate, U entries at a time
 // with all their (idx, val) loads issued before the REDs (the compiler may not hoist loads above
 // a RED it cannot prove does not alias them, which would serialise one L2 round trip per entry).
-template <int U>
+template <int U, bool WILD = false>
 __device__ __forceinline__ void scatter_strided(float *sv, const int32_t *idx, const float *val, int64_t k0,
                                                 int64_t end, int64_t stride, float d) {
   for (int64_t k = k0; k < end; k += stride * U) {
@@ -78,9 +97,7 @@ __device__ __forceinline__ void scatter_strided(float *sv, const int32_t *idx, c
       id[u] = kk < end ? __ldcg(idx + kk) : -1;
       v[u] = kk < end ? val_cg(val, kk) : 0.f;
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (id[u] >= 0) red_add(sv + id[u], v[u] * d);
+    scatter_regs<WILD, U>(sv, id, v, d);
   }
 }
 
@@ -194,7 +211,7 @@ __global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b
 // ----------------------------------------------------------------------------------------------
 // Register-resident CTA kernel (first version, kept for comparison): E entries per thread held
 // in registers between the gather-dot and the scatter.
-template <int FORM, int T, int E>
+template <int FORM, int T, int E, bool WILD = false>
 __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
   constexpr int NW = T / 32;
   __shared__ float s_red[NW];
@@ -251,10 +268,8 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
     __syncthreads();
     const float d = scatter_scale<FORM>(s_delta);
     if (d != 0.f || b.dry) {  // dry probe: same traffic, adds +0.0f (state unchanged)
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
+      scatter_regs<WILD, E>(a.sv, id, v, d);
+      scatter_strided<4, WILD>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
     }
   }
 }
@@ -277,11 +292,18 @@ __device__ __forceinline__ void red_add_v4(float *p, float4 v) {
                : "memory");
 }
 
-template <int T>
-__device__ __forceinline__ void head_flush(float *sv, float *s_acc, int H, int dry) {
+template <int T, bool SNAP>
+__device__ __forceinline__ void head_flush(float *sv, float *s_acc, float *s_w, int H, int dry) {
   float4 *a4 = reinterpret_cast<float4 *>(s_acc);
+  float4 *w4 = reinterpret_cast<float4 *>(s_w);
   for (int i = threadIdx.x; i < H / 4; i += T) {
     const float4 v = a4[i];
+    if (SNAP) {
+      // refresh the CTA's view of the head: L2 value (every flushed update) + own pending part,
+      // read BEFORE this CTA's RED of the pending part is issued (same thread, same address: ordered)
+      const float4 l = __ldcg(reinterpret_cast<const float4 *>(sv) + i);
+      w4[i] = make_float4(l.x + v.x, l.y + v.y, l.z + v.z, l.w + v.w);
+    }
     if (dry || v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f) {
       red_add_v4(sv + 4 * i, v);
       a4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -289,16 +311,21 @@ __device__ __forceinline__ void head_flush(float *sv, float *s_acc, int H, int d
   }
 }
 
-template <int FORM, int T, int E>
+template <int FORM, int T, int E, bool SNAP>
 __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
   constexpr int NW = T / 32;
   extern __shared__ float4 s_dyn[];
   float *s_acc = reinterpret_cast<float *>(s_dyn);
+  float *s_w = s_acc + H;  // SNAP: the CTA's view of the head (refreshed at every flush)
   __shared__ float s_red[NW];
   __shared__ float s_delta;
   __shared__ unsigned int s_ticket;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int i = tid; i < H; i += T) s_acc[i] = 0.f;
+  if (SNAP) {
+    __syncthreads();
+    head_flush<T, true>(a.sv, s_acc, s_w, H, 0);  // initial view (nothing pending yet)
+  }
   int since = 0;
   for (;;) {
     if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
@@ -324,8 +351,11 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (id[e] >= 0) {
-        float w = ld_sv(a.sv + id[e]);
-        if (id[e] < H) w += s_acc[id[e]];
+        float w;
+        if (SNAP)
+          w = id[e] < H ? s_w[id[e]] + s_acc[id[e]] : ld_sv(a.sv + id[e]);
+        else
+          w = ld_sv(a.sv + id[e]) + (id[e] < H ? s_acc[id[e]] : 0.f);
         acc = fmaf(w, v[e], acc);
       }
     for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
@@ -334,8 +364,11 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
         const int64_t k = base + (int64_t)e * T + tid;
         if (k < end) {
           const int32_t j = __ldcg(a.idx + k);
-          float w = ld_sv(a.sv + j);
-          if (j < H) w += s_acc[j];
+          float w;
+          if (SNAP)
+            w = j < H ? s_w[j] + s_acc[j] : ld_sv(a.sv + j);
+          else
+            w = ld_sv(a.sv + j) + (j < H ? s_acc[j] : 0.f);
           acc = fmaf(w, val_cg(a.val, k), acc);
         }
       }
@@ -387,10 +420,10 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
     if (++since == flush) {
       since = 0;
       __syncthreads();
-      head_flush<T>(a.sv, s_acc, H, b.dry);
+      head_flush<T, SNAP>(a.sv, s_acc, s_w, H, b.dry);
     }
   }
-  head_flush<T>(a.sv, s_acc, H, b.dry);  // after the exit barrier: every smem atomic has landed
+  head_flush<T, false>(a.sv, s_acc, s_w, H, b.dry);  // after the exit barrier: every pending update is final
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -515,7 +548,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_split(EpochArgs a, BinArgs b, Sp
 }
 
 // ----------------------------------------------------------------------------------------------
-template <int FORM, int G, int E>
+template <int FORM, int G, int E, bool WILD = false>
 __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
   constexpr int CPW = 32 / G;  // coordinates per warp per ticket
   const int lane = threadIdx.x & 31;
@@ -570,10 +603,8 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
     }
     d = scatter_scale<FORM>(__shfl_sync(0xffffffffu, d, sub * G));
     if (d != 0.f || b.dry) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
+      scatter_regs<WILD, E>(a.sv, id, v, d);
+      scatter_strided<4, WILD>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
     }
   }
 }
@@ -903,7 +934,7 @@ __global__ void k_partition_export(Perm p, int64_t count, int32_t k, int32_t *ow
 // To keep the GPU busy anyway, each one is split across a cluster of CL CTAs: every CTA takes a
 // contiguous slice, partial dots meet in CTA 0's shared memory over DSMEM, CTA 0 computes Δ, and
 // every CTA scatters its slice.  Two cluster barriers per coordinate.
-template <int FORM, int CL, int T, int E>
+template <int FORM, int CL, int T, int E, bool WILD = false>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(EpochArgs a, BinArgs b) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -975,10 +1006,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
     cluster.sync();
     const float d = scatter_scale<FORM>(*delta0);
     if (d != 0.f) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
+      scatter_regs<WILD, E>(a.sv, id, v, d);
+      scatter_strided<4, WILD>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
     }
   }
 }
@@ -1019,13 +1048,28 @@ void *kernel_for(int lanes, int plain) {
   }
 }
 
+// options.wild: the plain kernel of each bin with the non-atomic scatter (PASSCoDe-Wild comparison)
+template <int FORM>
+void *kernel_wild(int lanes) {
+  switch (lanes) {
+    case 8: return (void *)k_epoch_group<FORM, 8, kGrpE8, true>;
+    case 16: return (void *)k_epoch_group<FORM, 16, 4, true>;
+    case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32, true>;
+    case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE, true>;
+    default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE, true>;
+  }
+}
+
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
+  if (c->opt.wild) return c->form == SCD_PRIMAL ? kernel_wild<SCD_PRIMAL>(b.lanes) : kernel_wild<SCD_DUAL>(b.lanes);
   if (b.split && b.lanes == kLanesCta)
     return c->form == SCD_PRIMAL ? (void *)k_epoch_split<SCD_PRIMAL, kCtaT, kCtaE>
                                  : (void *)k_epoch_split<SCD_DUAL, kCtaT, kCtaE>;
   if (b.head > 0 && b.lanes == kLanesCta)
-    return c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE>
-                                 : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE>;
+    return c->head_snap ? (c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE, true>
+                                                 : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true>)
+                        : (c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE, false>
+                                                 : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false>);
   return c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
 }
 
@@ -1064,6 +1108,10 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   // caps fall back to the plain 8-lane kernel, and caps below 4 to one warp per coordinate.
   if (b.lanes == 8 && b.cap > 0 && b.cap < kCombT / 8) b.plain = 1;
   if (b.lanes == 8 && b.cap > 0 && b.cap < 4) b.lanes = 32;
+  if (c->opt.wild) {  // plain kernels only (no head / CTA combining, no die split)
+    b.plain = 1;
+    b.head = b.split = 0;
+  }
   if (b.lanes != kLanesCta) b.head = b.split = 0;
   if (b.split) b.head = 0;
   void *fn = bin_kernel(c, b);
@@ -1076,7 +1124,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
     if (block < 32) block = 32;
   }
-  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head : 0;
+  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head * (c->head_snap ? 2 : 1) : 0;
   if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
@@ -1133,7 +1181,7 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
     sa.nosync = c->split_nosync ? 1 : 0;
     args = args_split;
   }
-  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head : 0;
+  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head * (c->head_snap ? 2 : 1) : 0;
   SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(b.block), args, smem, s));
   return SCD_OK;
 }

@@ -37,7 +37,7 @@ class Options(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("n_global", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_comm", C.c_void_p), ("stream", C.c_void_p), ("deterministic", C.c_int32),
                 ("max_inflight", C.c_int32), ("recompute_every", C.c_int32), ("validate", C.c_int32),
-                ("profile", C.c_int32)]
+                ("profile", C.c_int32), ("wild", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -139,7 +139,7 @@ class Solver:
     def __init__(self, ptr, idx, val, n_rows: int, n_cols: int, y, lam: float, form: str = "dual", *,
                  seed: int = 0, deterministic: bool = False, max_inflight: int = 0, n_global: int = 0,
                  rank: int = 0, world: int = 1, nccl_comm=None, stream=None, validate: bool = True,
-                 profile: bool = False, recompute_every: int = 0):
+                 profile: bool = False, recompute_every: int = 0, wild: bool = False):
         L = lib()
         self._form = PRIMAL if form == "primal" else DUAL
         if form not in ("primal", "dual"):
@@ -166,6 +166,7 @@ class Solver:
         o.recompute_every = recompute_every
         o.validate = int(validate)
         o.profile = int(profile)
+        o.wild = int(wild)
         h = C.c_void_p()
         _check(L.scd_create(C.byref(m), yy, my, float(lam), self._form, C.byref(o), C.byref(h)))
         self._h = h

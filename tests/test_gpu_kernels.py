@@ -92,3 +92,28 @@ def test_die_split_kernel_convergence(c3p, monkeypatch):
     assert info["die_lat"][1] > 1.25 * info["die_lat"][0]
     assert 0 < info["split_nnz0"] < info["nnz"]
     assert any(b["split"] for b in info["bins"])
+
+
+def test_wild_variant_loses_updates(c3p):
+    """the non-atomic ("wild") scatter reproduces PASSCoDe-Wild's behaviour (P:164,
+    P:254): concurrent updates of the shared vector are lost, so w̄ drifts away from Aᵀα and the
+    duality gap (from scratch, on α) stalls, while the atomic path keeps w̄ = Aᵀα within fp32 drift
+    and reaches the optimum."""
+    d, pr, hist = c3p
+    A = pr.A()
+    out = {}
+    for wild in (False, True):
+        s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=4, wild=wild)
+        assert all(b["head"] == 0 for b in s.info()["bins"]) or not wild
+        for t in range(1, E + 1):
+            s.epoch(t)
+        g = s.duality_gap()
+        a = s.get_model().astype(np.float64)
+        wbar = s.get_shared().astype(np.float64)
+        s.close()
+        v = A.T @ a
+        out[wild] = (g, np.abs(wbar - v).max() / np.abs(v).max())
+    print("atomic gap %.2e drift %.2e | wild gap %.2e drift %.2e" % (*out[False], *out[True]))
+    assert out[False][1] <= 1e-4 and out[False][0] <= 1e-5
+    assert out[True][1] > 10 * out[False][1]
+    assert out[True][0] > 10 * out[False][0]
