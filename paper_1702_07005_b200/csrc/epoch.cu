@@ -1146,9 +1146,17 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   if (b.head > 0) {
     // pending head updates of `flush` coordinates per CTA are in flight as far as other CTAs are
     // concerned: grid * flush <= cap.  SCD_HEAD_FLUSH overrides (experiments only).
-    int64_t f = b.cap > 0 ? b.cap / b.grid : 16;
+    // With the shared-memory view of the head (head_snap) a read may also miss what other CTAs
+    // flushed since the CTA's last refresh: grid * flush more.
+    const int64_t k = c->head_snap ? 2 : 1;
+    int64_t f = b.cap > 0 ? b.cap / (b.grid * k) : 16;
     if (const char *e = getenv("SCD_HEAD_FLUSH")) f = atoi(e);
     if (f > 64) f = 64;
+    if (f < 2 && c->head_snap) {  // no room for the view: plain head kernel
+      c->head_snap = false;
+      bin_launch_shape(c, b);
+      return;
+    }
     if (f < 2) {  // no combining possible under the cap: plain CTA kernel
       b.head = 0;
       b.flush = 0;
