@@ -304,9 +304,15 @@ __device__ __forceinline__ void head_flush(float *sv, float *s_acc, float *s_w, 
       const float4 l = __ldcg(reinterpret_cast<const float4 *>(sv) + i);
       w4[i] = make_float4(l.x + v.x, l.y + v.y, l.z + v.z, l.w + v.w);
     }
-    if (dry || v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f) {
-      red_add_v4(sv + 4 * i, v);
-      a4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // dry probe: the pending array starts at -0.0f and the scatter adds +0.0f (non-negative values),
+    // which turns a touched entry into +0.0f, so the probe flushes exactly the touched float4s
+    const bool touched = dry ? (__float_as_uint(v.x) != 0x80000000u || __float_as_uint(v.y) != 0x80000000u ||
+                                __float_as_uint(v.z) != 0x80000000u || __float_as_uint(v.w) != 0x80000000u)
+                             : (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f);
+    if (touched) {
+      red_add_v4(sv + 4 * i, v);  // dry: adds +-0.0f, state unchanged
+      const float z = dry ? -0.f : 0.f;
+      a4[i] = make_float4(z, z, z, z);
     }
   }
 }
@@ -321,7 +327,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
   __shared__ float s_delta;
   __shared__ unsigned int s_ticket;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int i = tid; i < H; i += T) s_acc[i] = 0.f;
+  for (int i = tid; i < H; i += T) s_acc[i] = b.dry ? -0.f : 0.f;
   if (SNAP) {
     __syncthreads();
     head_flush<T, true>(a.sv, s_acc, s_w, H, 0);  // initial view (nothing pending yet)
@@ -1279,19 +1285,20 @@ scd_status tune_shared_layout(scd_ctx *c) {
   if (bi < 0) return SCD_OK;
   Bin &b = c->bins[bi];
   cudaStream_t s = c->stream;
-  const int unit = 1;
   const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;
-  const int64_t probe = std::min<int64_t>(b.count, (int64_t)b.grid * cpc * 32);
+  const int64_t probe = std::min<int64_t>(b.count, (int64_t)b.grid * cpc * 16);
   SCD_CK(c, cudaMemsetAsync(c->sv_base, 0, sizeof(float) * (size_t)(c->n_shared + kMaxSvOffsetFloats), s));
-  cudaEvent_t e0, e1;
-  SCD_CK(c, cudaEventCreate(&e0));
-  SCD_CK(c, cudaEventCreate(&e1));
-  double best_ms = 1e30;
-  int64_t best = 0;
-  c->n_probe = 0;
-  for (int ci = 0; ci < kSvCandidates; ++ci) {
-    const int64_t off = kSvCandidateBytes[ci] / 4;
-    c->sv = c->sv_base + off;
+  // all probe launches enqueued back to back between events (one warm-up, then kReps per candidate
+  // in round-robin order so slow drifts hit every candidate alike); one synchronisation at the end
+  constexpr int kReps = 2;
+  const int nl = 1 + kSvCandidates * kReps;
+  std::vector<cudaEvent_t> ev(nl + 1);
+  for (auto &e : ev) SCD_CK(c, cudaEventCreate(&e));
+  SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices, s));
+  SCD_CK(c, cudaEventRecord(ev[0], s));
+  for (int l = 0; l < nl; ++l) {
+    const int ci = l == 0 ? 0 : (l - 1) % kSvCandidates;
+    c->sv = c->sv_base + kSvCandidateBytes[ci] / 4;
     EpochArgs a = make_args(c);
     BinArgs ba;
     ba.list = b.list;
@@ -1299,31 +1306,32 @@ scd_status tune_shared_layout(scd_ctx *c) {
     ba.hi = probe;
     ba.perm = make_perm(c->opt.seed ^ 0x5052424Full, 0xFFFFFFFEu, b.stream_id, b.count);
     ba.dry = 1;
-    float ms_min = 1e30f;
-    for (int rep = 0; rep < 2; ++rep) {
-      ba.counter = c->counters + rep;
-      SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2, s));
-      SCD_CK(c, cudaMemsetAsync(c->counters + kMaxBins * kMaxSlices, 0, sizeof(unsigned int) * 2, s));
-      SCD_CK(c, cudaEventRecord(e0, s));
-      scd_status st = launch_bin(c, b, a, ba, (int64_t)b.grid * unit, s);
-      if (st != SCD_OK) return st;
-      SCD_CK(c, cudaEventRecord(e1, s));
-      SCD_CK(c, cudaEventSynchronize(e1));
-      float ms = 0.f;
-      SCD_CK(c, cudaEventElapsedTime(&ms, e0, e1));
-      ms_min = std::min(ms_min, ms);
-      ++c->launches;
-    }
-    c->probe_ms[c->n_probe++] = ms_min;
-    if (ms_min < best_ms) {
-      best_ms = ms_min;
-      best = off;
-    }
+    ba.counter = c->counters + l % (kMaxBins * kMaxSlices);
+    if (l > 0 && l % (kMaxBins * kMaxSlices) == 0)
+      SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices, s));
+    scd_status st = launch_bin(c, b, a, ba, (int64_t)b.grid, s);
+    if (st != SCD_OK) return st;
+    SCD_CK(c, cudaEventRecord(ev[l + 1], s));
+    ++c->launches;
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  c->sv = c->sv_base + best;
-  c->sv_offset_bytes = best * 4;
+  SCD_CK(c, cudaEventSynchronize(ev[nl]));
+  std::vector<float> best_of(kSvCandidates, 1e30f);
+  for (int l = 1; l < nl; ++l) {
+    float ms = 0.f;
+    SCD_CK(c, cudaEventElapsedTime(&ms, ev[l], ev[l + 1]));
+    const int ci = (l - 1) % kSvCandidates;
+    best_of[ci] = std::min(best_of[ci], ms);
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices, s));
+  int best = 0;
+  c->n_probe = 0;
+  for (int ci = 0; ci < kSvCandidates; ++ci) {
+    c->probe_ms[c->n_probe++] = best_of[ci];
+    if (best_of[ci] < best_of[best]) best = ci;
+  }
+  c->sv = c->sv_base + kSvCandidateBytes[best] / 4;
+  c->sv_offset_bytes = kSvCandidateBytes[best];
   return SCD_OK;
 }
 
