@@ -79,7 +79,7 @@ __device__ __forceinline__ uint64_t perm_apply(const Perm &p, uint64_t j) {
 // Context
 // ------------------------------------------------------------------------------------------
 constexpr int kLanesCta = 256;       // bin kind: one CTA of 256 threads per coordinate
-constexpr int kClusterCtas = 8;      // portable cluster size
+constexpr int kClusterCtas = 8;      // largest cluster size used (portable); the bin's `cl` picks 2, 4 or 8
 constexpr int kClusterThreads = 512;
 constexpr int kLanesCluster = kClusterCtas * kClusterThreads;  // bin kind: one 8-CTA cluster per coordinate
 
@@ -91,6 +91,7 @@ struct Bin {
   int head = 0;              // CTA bins: > 0 = head-combining kernel over sv[0, head) (k_epoch_cta_head)
   int flush = 0;             // head kernel: coordinates per CTA between flushes of the pending head
   int split = 0;             // CTA bins: 1 = die-split kernel (k_epoch_split, die.cu)
+  int cl = kClusterCtas;     // cluster bin: CTAs per cluster (one coordinate per cluster)
   int64_t count = 0, nnz = 0;
   int32_t *list = nullptr;   // device, coordinate ids ascending
   int grid = 0, block = 0;

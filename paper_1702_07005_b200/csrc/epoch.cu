@@ -1044,7 +1044,7 @@ void *kernel_for(int lanes, int plain) {
     case 16:
       return group_kind() == 1 ? (void *)k_epoch_group_pipe<FORM, 16, 4, 4> : (void *)k_epoch_group<FORM, 16, 4>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
-    case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE>;
+    case kLanesCluster: return nullptr;  // cluster_kernel(): depends on the bin's cluster size
     default: {
       // register-resident kernel by default (measured equal-or-faster and half the coordinates in
       // flight); SCD_CTA_KERNEL=stream selects the two-pass streaming variant
@@ -1061,12 +1061,26 @@ void *kernel_wild(int lanes) {
     case 8: return (void *)k_epoch_group<FORM, 8, kGrpE8, true>;
     case 16: return (void *)k_epoch_group<FORM, 16, 4, true>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32, true>;
-    case kLanesCluster: return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE, true>;
+    case kLanesCluster: return nullptr;
     default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE, true>;
   }
 }
 
+template <int FORM, bool WILD>
+void *cluster_kernel(int cl) {
+  switch (cl) {
+    case 2: return (void *)k_epoch_cluster<FORM, 2, kClusterThreads, kClE, WILD>;
+    case 4: return (void *)k_epoch_cluster<FORM, 4, kClusterThreads, kClE, WILD>;
+    default: return (void *)k_epoch_cluster<FORM, 8, kClusterThreads, kClE, WILD>;
+  }
+}
+
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
+  if (b.lanes == kLanesCluster) {
+    if (c->form == SCD_PRIMAL)
+      return c->opt.wild ? cluster_kernel<SCD_PRIMAL, true>(b.cl) : cluster_kernel<SCD_PRIMAL, false>(b.cl);
+    return c->opt.wild ? cluster_kernel<SCD_DUAL, true>(b.cl) : cluster_kernel<SCD_DUAL, false>(b.cl);
+  }
   if (c->opt.wild) return c->form == SCD_PRIMAL ? kernel_wild<SCD_PRIMAL>(b.lanes) : kernel_wild<SCD_DUAL>(b.lanes);
   if (b.split && b.lanes == kLanesCta)
     return c->form == SCD_PRIMAL ? (void *)k_epoch_split<SCD_PRIMAL, kCtaT, kCtaE>
@@ -1120,6 +1134,12 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   }
   if (b.lanes != kLanesCta) b.head = b.split = 0;
   if (b.split) b.head = 0;
+  if (b.lanes == kLanesCluster) {
+    // cluster size: large clusters split one very long coordinate over more SMs, small ones keep
+    // more coordinates in flight; SCD_CLUSTER = 2|4|8 overrides
+    static const int env_cl = getenv("SCD_CLUSTER") ? atoi(getenv("SCD_CLUSTER")) : 0;
+    b.cl = (env_cl == 2 || env_cl == 4 || env_cl == 8) ? env_cl : kClusterCtas;
+  }
   void *fn = bin_kernel(c, b);
   const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
@@ -1135,10 +1155,10 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
   if (occ < 1) occ = 1;
-  const int per_launch_unit = clus ? kClusterCtas : 1;           // CTAs per coordinate slot
+  const int per_launch_unit = clus ? b.cl : 1;                    // CTAs per coordinate slot
   const int coords_per_cta = group ? block / b.lanes : 1;
   int64_t slots = (int64_t)c->nsm * occ / per_launch_unit;        // resident coordinate slots
-  if (clus && slots > (int64_t)c->nsm / kClusterCtas * occ) slots = (int64_t)c->nsm / kClusterCtas * occ;
+  if (clus && slots > (int64_t)c->nsm / b.cl * occ) slots = (int64_t)c->nsm / b.cl * occ;
   int64_t units = slots;                                          // CTAs (or clusters)
   if (b.cap > 0) {  // staleness cap
     int64_t u = (b.cap + coords_per_cta - 1) / coords_per_cta;
@@ -1249,7 +1269,7 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.count);
       ba.dry = 0;
       const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;  // coordinates per CTA (or cluster)
-      const int unit = b.lanes == kLanesCluster ? kClusterCtas : 1;
+      const int unit = b.lanes == kLanesCluster ? b.cl : 1;
       const int64_t need = ((ba.hi - ba.lo) + cpc - 1) / cpc;
       int64_t grid = b.grid / unit;
       if (grid > need) grid = need;
