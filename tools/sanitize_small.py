@@ -1,6 +1,8 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer (memcheck / racecheck):
-deterministic and asynchronous epochs (CTA, sub-warp, combining, cluster bins), empty rows/cols,
-implicit values, gap/objective, aggregation (group and 1-rank NCCL), transpose, permutation."""
+deterministic and asynchronous epochs (CTA, sub-warp, combining, cluster bins), the head-combining
+CTA kernel (plain and with the shared-memory view), the die-split kernel, the wild scatter, empty
+rows/cols, implicit values, gap/objective, aggregation (group and 1-rank NCCL), transpose,
+permutation."""
 import os
 import sys
 
@@ -61,4 +63,18 @@ for s in a:
     s.epoch(1)
 print("group", scd.aggregate_group(a, "optimal"))
 assert np.array_equal(np.sort(scd.permutation(1, 2, 1000)), np.arange(1000))
+for form in ("dual", "primal"):
+    print("wild", form, run(d, form, wild=True), flush=True)
+# webspam-shaped rows (C3 prefix, λN = 350 as in the full C3) put every row in the CTA bin with a grid
+# covering every SM: head-combining kernel, its shared-memory view, and the die-split kernel
+c3 = synth.gen_host(synth.CONFIGS["C3"].with_rows(1500))
+c3["lam"] = 350.0 / 1500
+for env in ({}, {"SCD_HEAD_SNAP": "1", "SCD_HEAD_FLUSH": "2"}, {"SCD_DIE_SPLIT": "1"}):
+    os.environ.update(env)
+    s = scd.Solver(c3["ptr"], c3["idx"], c3["val"], 1500, c3["n_cols"], c3["y"], c3["lam"], "dual", seed=3)
+    inf = s.info()
+    s.close()
+    print("c3 prefix", env, inf["bins"][0], "die_split", inf["die_split"], run(c3, "dual"), flush=True)
+    for k in env:
+        del os.environ[k]
 print("sanitize_small done")
