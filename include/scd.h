@@ -194,6 +194,8 @@ typedef struct {
   int32_t n_die_sm[2];    /* SMs found on each die by the create-time probe */
   float die_lat[2];       /* probe: near / far atomic round-trip latency (SM cycles) */
   int64_t split_nnz0;     /* die split: stored entries whose shared-vector element is homed on die 0 */
+  int32_t bin_hot[4];     /* per bin: > 0 = hot-set kernel with this many hot shared-vector entries (hot.cu) */
+  double hot_cover;       /* share of the hot bin's stored entries that fall on a hot entry */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

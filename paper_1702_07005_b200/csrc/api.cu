@@ -55,6 +55,8 @@ void free_ctx(scd_ctx *c) {
   for (int i = 0; i < kMaxBins; ++i) cudaFree(c->bins[i].list);
   cudaFree(c->counters);
   cudaFree(c->sm_die);
+  cudaFree(c->hot_idx);
+  cudaFree(c->hot_ids);
   cudaFree(c->split_mid);
   cudaFree(c->split_idx);
   cudaFree(c->split_val);
@@ -396,6 +398,7 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->die_lat[0] = c->die_lat[0];
   info->die_lat[1] = c->die_lat[1];
   info->split_nnz0 = c->split_nnz0;
+  info->hot_cover = c->hot_cover;
   info->inflight_cap = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i) {
     info->bin_cap[i] = c->bins[i].cap;
@@ -403,6 +406,7 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
     info->bin_head[i] = c->bins[i].head;
     info->bin_flush[i] = c->bins[i].flush;
     info->bin_split[i] = c->bins[i].split;
+    info->bin_hot[i] = c->bins[i].hot;
     if (c->bins[i].cap > info->inflight_cap) info->inflight_cap = c->bins[i].cap;
   }
   return SCD_OK;

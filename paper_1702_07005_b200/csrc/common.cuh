@@ -92,6 +92,7 @@ struct Bin {
   int flush = 0;             // head kernel: coordinates per CTA between flushes of the pending head
   int split = 0;             // CTA bins: 1 = die-split kernel (k_epoch_split, die.cu)
   int cl = kClusterCtas;     // cluster bin: CTAs per cluster (one coordinate per cluster)
+  int hot = 0;               // 8-lane bin: > 0 = hot-set kernel with this many hot slots (hot.cu)
   int64_t count = 0, nnz = 0;
   int32_t *list = nullptr;   // device, coordinate ids ascending
   int grid = 0, block = 0;
@@ -148,6 +149,10 @@ struct scd_ctx {
   double tau_star = 0.0;   // smallest estimated staleness bound over the bins (layout.cu)
   // die-split epoch (die.cu): SM -> die map, each coordinate's entries reordered so
   // the ones whose shared-vector entry is homed in die 0's L2 come first
+  int32_t *hot_idx = nullptr;         // device [nnz]: re-encoded indices for the hot-set kernel (hot.cu)
+  int32_t *hot_ids = nullptr;         // device [K]: shared-vector index of each hot slot
+  bool hot_view = false;              // hot-set kernel also keeps a per-CTA view of the hot values
+  double hot_cover = 0.0;             // share of the bin's entries that are hot
   bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)
   bool die_split = false;
   uint8_t *sm_die = nullptr;          // device [kMaxSm]: die of each SM id
@@ -206,6 +211,9 @@ scd_status tune_shared_layout(scd_ctx *c);
 void bin_launch_shape(scd_ctx *c, Bin &b);
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
 scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);
+
+// hot.cu ---------------------------------------------------------------------------------------
+scd_status setup_hot(scd_ctx *c);
 
 // die.cu ---------------------------------------------------------------------------------------
 scd_status setup_die_split(scd_ctx *c);

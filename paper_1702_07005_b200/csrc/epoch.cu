@@ -878,6 +878,128 @@ __global__ void __launch_bounds__(T) k_epoch_group_comb(EpochArgs a, BinArgs b) 
 }
 
 // ----------------------------------------------------------------------------------------------
+// Hot-set sub-warp kernel for short coordinates (criteo-shaped one-hot rows).  A few thousand
+// shared-vector entries carry most of the stored entries (C5: the 4096 most frequent features hold
+// 79% of them) and every row updates some of them, so their L2 lines serialise.  At create
+// (hot.cu) the K most frequent entries get a slot and a private copy of the bin's indices is
+// re-encoded: id >= 0 = tail entry (shared-vector index), id < 0 = hot entry (slot = id & 0x7fffffff).
+// Each CTA keeps its pending updates of the hot entries in shared memory (s_pend, CAS-loop atomics:
+// the CTA's rows update them concurrently) and, with VIEW, a copy of their values refreshed at every
+// flush; the warps run their rows without any CTA barrier and meet every F row batches to flush
+// (one RED per touched hot entry) — so a hot line takes one RED per CTA per F batches instead of
+// one per row.  Pending (and, with VIEW, view age) are extra staleness, bounded by the schedule:
+// grid * rows per CTA * (1 + F * (VIEW ? 2 : 1)) <= cap.
+struct HotArgs {
+  const int32_t *idx;      // re-encoded entries of the bin's coordinates (same offsets as EpochArgs::ptr)
+  const int32_t *hot_ids;  // [K]: shared-vector index of each hot slot
+  int K;                   // hot slots (multiple of 4)
+  int F;                   // row batches per warp between flushes
+};
+
+template <int FORM, int G, int E, bool VIEW>
+__global__ void __launch_bounds__(256) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
+  constexpr int CPW = 32 / G;
+  const unsigned FULL = 0xffffffffu;
+  extern __shared__ float4 s_dyn[];
+  float *s_pend = reinterpret_cast<float *>(s_dyn);  // [K] pending updates of the hot entries
+  float *s_aux = s_pend + h.K;                       // [K] VIEW: values; else: int32 shared-vector index
+  int32_t *s_hid = reinterpret_cast<int32_t *>(s_aux);
+  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+  for (int i = threadIdx.x; i < h.K; i += blockDim.x) {
+    s_pend[i] = b.dry ? -0.f : 0.f;
+    const int32_t j = __ldg(h.hot_ids + i);
+    if (VIEW)
+      s_aux[i] = ld_sv(a.sv + j);
+    else
+      s_hid[i] = j;
+  }
+  __syncthreads();
+  bool more = true;  // warp-uniform: the warp still gets tickets
+  for (;;) {
+    for (int it = 0; it < h.F && more; ++it) {
+      unsigned int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(b.counter, (unsigned)CPW);
+      t0 = __shfl_sync(FULL, t0, 0);
+      if (b.lo + (int64_t)t0 >= b.hi) {
+        more = false;
+        break;
+      }
+      int64_t cl = -1;
+      if (lane < CPW && b.lo + (int64_t)t0 + lane < b.hi) cl = bin_coord(b, b.lo + t0 + lane);
+      const int64_t c = __shfl_sync(FULL, cl, sub);
+      int64_t beg = 0, end = 0;
+      if (c >= 0) {
+        beg = __ldg(a.ptr + c);
+        end = __ldg(a.ptr + c + 1);
+      }
+      int32_t id[E];
+      float v[E];
+      unsigned valid = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t k = beg + (int64_t)e * G + gl;
+        id[e] = 0;
+        v[e] = 0.f;
+        if (k < end) {
+          id[e] = __ldcs(h.idx + k);
+          v[e] = val_cs(a.val, k);
+          valid |= 1u << e;
+        }
+      }
+      float w[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        w[e] = 0.f;
+        if (valid >> e & 1) {
+          if (id[e] >= 0) {
+            w[e] = ld_sv(a.sv + id[e]);
+          } else {
+            const int sl = id[e] & 0x7fffffff;
+            w[e] = (VIEW ? s_aux[sl] : ld_sv(a.sv + s_hid[sl])) + s_pend[sl];
+          }
+        }
+      }
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fmaf(w[e], v[e], acc);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+      float d = 0.f;
+      if (c >= 0 && gl == 0) {  // group leader: single writer of x[c] (c10)
+        const float xc = a.x[c];
+        d = coord_delta<FORM>(acc, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f, a.lam, a.lamN);
+        if (!b.dry) a.x[c] = xc + d;
+        if (b.dry) d = 0.f;
+      }
+      d = scatter_scale<FORM>(__shfl_sync(FULL, d, sub * G));
+      if (d != 0.f || b.dry) {  // dry probe: same traffic, adds +0.0f
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (valid >> e & 1) {
+            if (id[e] >= 0)
+              red_add(a.sv + id[e], v[e] * d);
+            else
+              atomicAdd(s_pend + (id[e] & 0x7fffffff), v[e] * d);
+          }
+      }
+    }
+    const bool any = __syncthreads_or(more);
+    for (int i = threadIdx.x; i < h.K; i += blockDim.x) {  // flush (and refresh the view)
+      const float p = s_pend[i];
+      const int32_t j = VIEW ? __ldg(h.hot_ids + i) : s_hid[i];
+      if (VIEW) s_aux[i] = ld_sv(a.sv + j) + p;  // read before this CTA's RED: own pending counted once
+      // dry probe: pending starts at -0.0f and a touched slot becomes +0.0f (non-negative values)
+      if (b.dry ? __float_as_uint(p) != 0x80000000u : p != 0.f) {
+        red_add(a.sv + j, p);
+        s_pend[i] = b.dry ? -0.f : 0.f;
+      }
+    }
+    __syncthreads();
+    if (!any) break;
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
 // Deterministic (debug) epoch: exactly Alg. 1's order with Alg. 2's arithmetic, one coordinate
 // at a time, fixed reduction tree (strided per-thread partials -> xor-shuffle tree -> 8 warp
 // partials summed in order).  Plain read-modify-write scatter: one coordinate in flight and
@@ -1076,6 +1198,11 @@ void *cluster_kernel(int cl) {
 }
 
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
+  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild) {
+    if (c->form == SCD_PRIMAL)
+      return c->hot_view ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, true> : (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false>;
+    return c->hot_view ? (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, true> : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false>;
+  }
   if (b.lanes == kLanesCluster) {
     if (c->form == SCD_PRIMAL)
       return c->opt.wild ? cluster_kernel<SCD_PRIMAL, true>(b.cl) : cluster_kernel<SCD_PRIMAL, false>(b.cl);
@@ -1120,6 +1247,54 @@ cudaEvent_t get_event(scd_ctx *c) {
 
 }  // namespace
 
+// Combined (deferred) updates — the head kernel's pending head, the hot-set kernel's pending hot
+// entries — are missed by other CTAs' reads for a whole window, so their windows are sized against
+// the bin's staleness bound itself: `inflight` coordinates in flight plus `inflight` * window * k
+// deferred ones <= SCD_COMBINE_BUDGET * τ_b (default 1.0; an explicit max_inflight replaces τ_b).
+// The in-flight cap keeps its 0.5 safety factor.  Measured (profiles/hot_sweep_r1.txt,
+// head_sweep_r1.txt): per-epoch gaps unchanged within 3% up to 2 τ, divergence beyond ~4 τ.
+//
+// The per-epoch rate also depends on how large a fraction of the epoch is stale at once: on a
+// 20 000-row C3 prefix a window of 5 rows per CTA (3 500 of 19 400 coordinates deferred) left the
+// gap 15x behind the sequential one after 4 epochs, so the deferred total is also kept <= 1/8 of the
+// bin's coordinates (never binding on the full-size configs).
+int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t k) {
+  static const double frac = getenv("SCD_COMBINE_BUDGET") ? atof(getenv("SCD_COMBINE_BUDGET")) : 1.0;
+  double budget = c->opt.max_inflight > 0 ? (double)b.cap : frac * b.tau;
+  budget = std::min(budget, (double)b.count / 8.0);
+  if (inflight < 1 || budget <= 0) return 0;
+  return (int64_t)((budget / (double)inflight - 1.0) / (double)k);
+}
+
+// Hot-set bin (k_epoch_group_hot): 256-thread CTAs, 32 rows in flight per CTA, window F batches.
+// The grid is lowered (in steps of one CTA per SM, not below two per SM) until F >= 6 fits the
+// budget: longer windows combine more and beat extra CTAs (profiles/hot_sweep_r1.txt).
+// SCD_HOT_F / SCD_HOT_CTAS (CTAs per SM) override (experiments).
+void hot_launch_shape(scd_ctx *c, Bin &b) {
+  void *fn = bin_kernel(c, b);
+  const size_t smem = 8 * (size_t)b.hot;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem);
+  if (occ < 1) occ = 1;
+  if (const char *e = getenv("SCD_HOT_CTAS")) occ = std::max(1, std::min(occ, atoi(e)));
+  const int64_t k = c->hot_view ? 2 : 1, rows = 256 / 8;
+  const int64_t need = (b.count + rows - 1) / rows;
+  int64_t grid = std::min<int64_t>((int64_t)c->nsm * occ, std::max<int64_t>(need, 1));
+  const char *fe = getenv("SCD_HOT_F");
+  while (!fe && combine_window(c, b, grid * rows, k) < 6 && grid > 2 * (int64_t)c->nsm) grid -= c->nsm;
+  int64_t F = std::max<int64_t>(1, std::min<int64_t>(64, combine_window(c, b, grid * rows, k)));
+  if (fe) F = std::max(1, atoi(fe));
+  if (!fe && F < 4) {  // too short a window to beat the CTA-combining kernel: use that instead
+    b.hot = 0;
+    bin_launch_shape(c, b);
+    return;
+  }
+  b.grid = (int)std::max<int64_t>(grid, 1);
+  b.block = 256;
+  b.flush = (int)F;
+}
+
 // Grid/block for a bin (used by build_schedule): persistent, sized to the SM count times the
 // kernel's residency, capped by max_inflight coordinates in flight.
 void bin_launch_shape(scd_ctx *c, Bin &b) {
@@ -1139,6 +1314,11 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
     // more coordinates in flight; SCD_CLUSTER = 2|4|8 overrides
     static const int env_cl = getenv("SCD_CLUSTER") ? atoi(getenv("SCD_CLUSTER")) : 0;
     b.cl = (env_cl == 2 || env_cl == 4 || env_cl == 8) ? env_cl : kClusterCtas;
+  }
+  if (b.hot > 0 && (b.lanes != 8 || c->opt.wild)) b.hot = 0;
+  if (b.hot > 0) {
+    hot_launch_shape(c, b);
+    return;
   }
   void *fn = bin_kernel(c, b);
   const bool group = (b.lanes <= 32);
@@ -1170,12 +1350,12 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   b.grid = (int)(units * per_launch_unit);
   b.block = block;
   if (b.head > 0) {
-    // pending head updates of `flush` coordinates per CTA are in flight as far as other CTAs are
-    // concerned: grid * flush <= cap.  SCD_HEAD_FLUSH overrides (experiments only).
-    // With the shared-memory view of the head (head_snap) a read may also miss what other CTAs
-    // flushed since the CTA's last refresh: grid * flush more.
+    // Pending head updates of `flush` coordinates per CTA are missed by other CTAs' reads, on top
+    // of the grid coordinates in flight: grid * (1 + flush * k) <= combined-update budget, k = 2
+    // with the shared-memory view (a read may also miss what others flushed since the CTA's last
+    // refresh).  SCD_HEAD_FLUSH overrides (experiments only).
     const int64_t k = c->head_snap ? 2 : 1;
-    int64_t f = b.cap > 0 ? b.cap / (b.grid * k) : 16;
+    int64_t f = combine_window(c, b, b.grid, k);
     if (const char *e = getenv("SCD_HEAD_FLUSH")) f = atoi(e);
     if (f > 64) f = 64;
     if (f < 2 && c->head_snap) {  // no room for the view: plain head kernel
@@ -1183,7 +1363,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
       bin_launch_shape(c, b);
       return;
     }
-    if (f < 2) {  // no combining possible under the cap: plain CTA kernel
+    if (f < 2) {  // no combining possible within the budget: plain CTA kernel
       b.head = 0;
       b.flush = 0;
       bin_launch_shape(c, b);
@@ -1200,7 +1380,16 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
   void *args_head[] = {&a, &ba, &H, &F};
   SplitArgs sa;
   void *args_split[] = {&a, &ba, &sa};
+  HotArgs ha;
+  void *args_hot[] = {&a, &ba, &ha};
   void **args = args_head;
+  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild) {
+    ha.idx = c->hot_idx;
+    ha.hot_ids = c->hot_ids;
+    ha.K = b.hot;
+    ha.F = b.flush;
+    args = args_hot;
+  }
   if (b.split) {
     sa.mid = c->split_mid;
     sa.idx = c->split_idx;
@@ -1215,7 +1404,8 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
     sa.nosync = c->split_nosync ? 1 : 0;
     args = args_split;
   }
-  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head * (c->head_snap ? 2 : 1) : 0;
+  const size_t smem = b.hot > 0 ? 8 * (size_t)b.hot
+                     : (b.head > 0 ? sizeof(float) * (size_t)b.head * (c->head_snap ? 2 : 1) : 0);
   SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(b.block), args, smem, s));
   return SCD_OK;
 }
@@ -1268,7 +1458,7 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       ba.counter = c->counters + sl * kMaxBins + i;
       ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.count);
       ba.dry = 0;
-      const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;  // coordinates per CTA (or cluster)
+      const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;  // coordinates per CTA (or cluster) per round
       const int unit = b.lanes == kLanesCluster ? b.cl : 1;
       const int64_t need = ((ba.hi - ba.lo) + cpc - 1) / cpc;
       int64_t grid = b.grid / unit;

@@ -255,6 +255,7 @@ scd_status build_schedule(scd_ctx *c) {
     int v = atoi(e);
     if (v >= 1 && v <= kMaxSlices) c->n_slices = v;
   }
+  if (scd_status st = setup_hot(c); st != SCD_OK) return st;
   // two ticket counters per (slice, bin): the second feeds die 1 of the die-split kernel
   SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices));
   return SCD_OK;
