@@ -914,74 +914,99 @@ __global__ void __launch_bounds__(256) k_epoch_group_hot(EpochArgs a, BinArgs b,
       s_hid[i] = j;
   }
   __syncthreads();
-  bool more = true;  // warp-uniform: the warp still gets tickets
+  // Software pipeline (as in k_epoch_group_pipe): while batch i gathers, reduces and scatters, the
+  // coordinates, offsets, scalars and entries of batch i+1 are already loaded.  Only batch i reads
+  // the shared vector, so the prefetch adds no staleness.
+  auto take = [&]() -> int64_t {  // warp-uniform: this lane's coordinate of the next batch, -1 = none
+    unsigned int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(b.counter, (unsigned)CPW);
+    t0 = __shfl_sync(FULL, t0, 0);
+    if (b.lo + (int64_t)t0 >= b.hi) return -2;  // slice exhausted (uniform)
+    int64_t cl = -1;
+    if (lane < CPW && b.lo + (int64_t)t0 + lane < b.hi) cl = bin_coord(b, b.lo + t0 + lane);
+    return __shfl_sync(FULL, cl, sub);
+  };
+  struct Batch {
+    int64_t c;
+    int32_t id[E];
+    float v[E];
+    unsigned valid;
+    float xc, nrm, yc;
+  };
+  auto load = [&](Batch &q, int64_t c) {
+    q.c = c;
+    q.valid = 0;
+    q.xc = q.nrm = q.yc = 0.f;
+    int64_t beg = 0, end = 0;
+    if (c >= 0) {
+      beg = __ldg(a.ptr + c);
+      end = __ldg(a.ptr + c + 1);
+      if (gl == 0) {
+        q.xc = a.x[c];  // this warp is the single writer of x[c]: the prefetched value is current
+        q.nrm = __ldg(a.norm + c);
+        if (FORM == SCD_DUAL) q.yc = __ldg(a.y + c);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t k = beg + (int64_t)e * G + gl;
+      q.id[e] = 0;
+      q.v[e] = 0.f;
+      if (k < end) {
+        q.id[e] = __ldcs(h.idx + k);
+        q.v[e] = val_cs(a.val, k);
+        q.valid |= 1u << e;
+      }
+    }
+  };
+  Batch cur, nxt;
+  int64_t cn = take();
+  bool more = cn != -2;  // warp-uniform: the warp holds a batch
+  if (more) load(cur, cn);
   for (;;) {
     for (int it = 0; it < h.F && more; ++it) {
-      unsigned int t0 = 0;
-      if (lane == 0) t0 = atomicAdd(b.counter, (unsigned)CPW);
-      t0 = __shfl_sync(FULL, t0, 0);
-      if (b.lo + (int64_t)t0 >= b.hi) {
-        more = false;
-        break;
-      }
-      int64_t cl = -1;
-      if (lane < CPW && b.lo + (int64_t)t0 + lane < b.hi) cl = bin_coord(b, b.lo + t0 + lane);
-      const int64_t c = __shfl_sync(FULL, cl, sub);
-      int64_t beg = 0, end = 0;
-      if (c >= 0) {
-        beg = __ldg(a.ptr + c);
-        end = __ldg(a.ptr + c + 1);
-      }
-      int32_t id[E];
-      float v[E];
-      unsigned valid = 0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int64_t k = beg + (int64_t)e * G + gl;
-        id[e] = 0;
-        v[e] = 0.f;
-        if (k < end) {
-          id[e] = __ldcs(h.idx + k);
-          v[e] = val_cs(a.val, k);
-          valid |= 1u << e;
-        }
-      }
+      // next batch: ticket + coordinates + entries (no shared-vector access)
+      cn = take();
+      const bool have_next = cn != -2;
+      if (have_next) load(nxt, cn);
+      // current batch: gather-dot
       float w[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         w[e] = 0.f;
-        if (valid >> e & 1) {
-          if (id[e] >= 0) {
-            w[e] = ld_sv(a.sv + id[e]);
+        if (cur.valid >> e & 1) {
+          if (cur.id[e] >= 0) {
+            w[e] = ld_sv(a.sv + cur.id[e]);
           } else {
-            const int sl = id[e] & 0x7fffffff;
+            const int sl = cur.id[e] & 0x7fffffff;
             w[e] = (VIEW ? s_aux[sl] : ld_sv(a.sv + s_hid[sl])) + s_pend[sl];
           }
         }
       }
       float acc = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc = fmaf(w[e], v[e], acc);
+      for (int e = 0; e < E; ++e) acc = fmaf(w[e], cur.v[e], acc);
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
       float d = 0.f;
-      if (c >= 0 && gl == 0) {  // group leader: single writer of x[c] (c10)
-        const float xc = a.x[c];
-        d = coord_delta<FORM>(acc, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f, a.lam, a.lamN);
-        if (!b.dry) a.x[c] = xc + d;
+      if (cur.c >= 0 && gl == 0) {  // group leader: single writer of x[c] (c10)
+        d = coord_delta<FORM>(acc, cur.xc, cur.nrm, cur.yc, a.lam, a.lamN);
+        if (!b.dry) a.x[cur.c] = cur.xc + d;
         if (b.dry) d = 0.f;
       }
       d = scatter_scale<FORM>(__shfl_sync(FULL, d, sub * G));
       if (d != 0.f || b.dry) {  // dry probe: same traffic, adds +0.0f
 #pragma unroll
         for (int e = 0; e < E; ++e)
-          if (valid >> e & 1) {
-            if (id[e] >= 0)
-              red_add(a.sv + id[e], v[e] * d);
+          if (cur.valid >> e & 1) {
+            if (cur.id[e] >= 0)
+              red_add(a.sv + cur.id[e], cur.v[e] * d);
             else
-              atomicAdd(s_pend + (id[e] & 0x7fffffff), v[e] * d);
+              atomicAdd(s_pend + (cur.id[e] & 0x7fffffff), cur.v[e] * d);
           }
       }
+      more = have_next;
+      if (have_next) cur = nxt;
     }
     const bool any = __syncthreads_or(more);
     for (int i = threadIdx.x; i < h.K; i += blockDim.x) {  // flush (and refresh the view)
