@@ -330,7 +330,7 @@ def main():
         hy.copy_(d["y"])
         n_ep = (ttg or {}).get("epochs") or 5
         times = []
-        for rep in range(3):
+        for rep in range(5):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             s2 = scd.Solver(hp, hi, hv, rows, cfg.n_cols, hy, cfg.lam, "dual", seed=3, validate=False)
@@ -344,6 +344,7 @@ def main():
         e_s = statistics.median(times)
         e2e = {"value": nnz * n_ep / e_s, "unit": "nnz/s", "h2d_bytes_per_step": int(8 * (rows + 1) + 8 * nnz + 4 * rows),
                "d2h_bytes_per_step": int(4 * rows), "epochs_per_step": n_ep, "seconds_per_step": e_s,
+               "seconds_per_rep": [round(x, 4) for x in times],
                "step": "scd_create from pinned host CSR (H2D) + epochs-to-gap-1e-4 + scd_get_model (D2H)"}
         del hp, hi, hv, hy
 

@@ -82,6 +82,29 @@ __device__ __forceinline__ void scatter_regs(float *sv, const int32_t *id, const
   }
 }
 
+// Partial dot over the entries k = k0 + j*stride (k < end) of a coordinate, U entries at a time:
+// all U (idx, val) loads, then all U gathers, then the FMAs (U independent round trips in flight).
+template <int U>
+__device__ __forceinline__ float dot_strided(const float *sv, const int32_t *idx, const float *val, int64_t k0,
+                                             int64_t end, int64_t stride) {
+  float acc = 0.f;
+  for (int64_t k = k0; k < end; k += stride * U) {
+    int32_t id[U];
+    float v[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t kk = k + (int64_t)u * stride;
+      id[u] = kk < end ? __ldcg(idx + kk) : -1;
+      v[u] = kk < end ? val_cg(val, kk) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = id[u] >= 0 ? ld_sv(sv + id[u]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = fmaf(w[u], v[u], acc);
+  }
+  return acc;
+}
+
 // Scatter of the entries k = k0 + j*stride (k < end) of a coordinate, U entries at a time
 // with all their (idx, val) loads issued before the REDs (the compiler may not hoist loads above
 // a RED it cannot prove does not alias them, which would serialise one L2 round trip per entry).
@@ -244,13 +267,7 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
     for (int e = 0; e < E; ++e)
       if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
     // remaining chunks of a long coordinate (re-read for the scatter; L2-resident by then)
-    for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
-#pragma unroll 4
-      for (int e = 0; e < E; ++e) {
-        const int64_t k = base + (int64_t)e * T + tid;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
-      }
-    }
+    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T);
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -269,7 +286,7 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
     const float d = scatter_scale<FORM>(s_delta);
     if (d != 0.f || b.dry) {  // dry probe: same traffic, adds +0.0f (state unchanged)
       scatter_regs<WILD, E>(a.sv, id, v, d);
-      scatter_strided<4, WILD>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
+      scatter_strided<8, WILD>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
     }
   }
 }
@@ -506,13 +523,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_split(EpochArgs a, BinArgs b, Sp
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
-#pragma unroll 4
-      for (int e = 0; e < E; ++e) {
-        const int64_t k = base + (int64_t)e * T + tid;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(s.idx + k)), val_cg(s.val, k), acc);
-      }
-    }
+    acc += dot_strided<8>(a.sv, s.idx, s.val, beg + (int64_t)T * E + tid, end, T);
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -548,7 +559,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_split(EpochArgs a, BinArgs b, Sp
 #pragma unroll
       for (int e = 0; e < E; ++e)
         if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      scatter_strided<4>(a.sv, s.idx, s.val, beg + (int64_t)T * E + tid, end, T, d);
+      scatter_strided<8>(a.sv, s.idx, s.val, beg + (int64_t)T * E + tid, end, T, d);
     }
   }
 }
@@ -591,13 +602,7 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    for (int64_t base = beg + (int64_t)G * E; base < end; base += (int64_t)G * E) {
-#pragma unroll 4
-      for (int e = 0; e < E; ++e) {
-        const int64_t k = base + (int64_t)e * G + gl;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
-      }
-    }
+    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     float d = 0.f;
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
     d = scatter_scale<FORM>(__shfl_sync(0xffffffffu, d, sub * G));
     if (d != 0.f || b.dry) {
       scatter_regs<WILD, E>(a.sv, id, v, d);
-      scatter_strided<4, WILD>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
+      scatter_strided<8, WILD>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
     }
   }
 }
@@ -690,13 +695,7 @@ __global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    for (int64_t base = beg + (int64_t)G * E; base < end; base += (int64_t)G * E) {
-#pragma unroll 4
-      for (int e = 0; e < E; ++e) {
-        const int64_t k = base + (int64_t)e * G + gl;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
-      }
-    }
+    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
     // (c) delta of batch i (group leader is the single writer of x[c], c10)
@@ -721,7 +720,7 @@ __global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b
 #pragma unroll
       for (int e = 0; e < E; ++e)
         if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      scatter_strided<4>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
+      scatter_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
     }
     // (f) coordinates of batch i+2, rotate
     const bool more = __any_sync(FULL, c_nxt >= 0);
@@ -1131,13 +1130,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
-#pragma unroll 4
-      for (int e = 0; e < E; ++e) {
-        const int64_t k = base + (int64_t)e * T + tid;
-        if (k < end) acc = fmaf(ld_sv(a.sv + __ldcg(a.idx + k)), val_cg(a.val, k), acc);
-      }
-    }
+    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T);
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -1160,7 +1153,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
     const float d = scatter_scale<FORM>(*delta0);
     if (d != 0.f) {
       scatter_regs<WILD, E>(a.sv, id, v, d);
-      scatter_strided<4, WILD>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
+      scatter_strided<8, WILD>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T, d);
     }
   }
 }
