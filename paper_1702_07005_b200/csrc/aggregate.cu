@@ -13,6 +13,17 @@
 //             γ̄ = (S_ydx - N S_x0dx - <Δw̄, w̄₀>/λ) / (||Δw̄||²/λ + N S_dxdx)
 //     zero denominator -> γ = 0 (c16)
 //   sv = sv₀ + γΔ ;  x_k = x₀_k + γΔx_k ;  the result becomes the next base point (c6).
+//
+// Two implementations of the exchange:
+//   NCCL   pack Δ_k, ncclAllReduce(Δ) + the worker scalars, dots, γ, apply (default for world > 1)
+//   fused  over peer memory (the K logical workers of scd_aggregate_group on one device, and
+//          world > 1 with SCD_P2P_AGG=1 through CUDA IPC over NVLink): each rank owns a shard of
+//          the shared vector; k_agg_reduce reads every worker's sv for the shard and forms Δ and
+//          the shard's <sv₀, Δ>, ||Δ||² in one pass (reduce-scatter fused with the dots);
+//          after the scalar all-reduce and γ, k_agg_apply writes sv₀ + γΔ of the shard straight
+//          into every worker's sv and sv₀ (all-gather fused with the axpy).
+#include <vector>
+
 #include "common.cuh"
 
 namespace scd {
@@ -85,6 +96,37 @@ __global__ void k_apply_shared(float *sv, float *sv0, const float *d, int64_t n,
   }
 }
 
+// Fused reduce-scatter + dots: shard [lo, hi) of Δ = Σ_k (sv_k - sv₀) from every worker's sv
+// (peer pointers), acc[3] += <sv₀, Δ>, acc[4] += ||Δ||² over the shard.
+__global__ void __launch_bounds__(kT) k_agg_reduce(const float *const *peer_sv, int K, const float *sv0, int64_t lo,
+                                                   int64_t hi, float *delta, double *acc) {
+  double a = 0.0, b = 0.0;
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    const float base = sv0[i];
+    float d = 0.f;
+    for (int k = 0; k < K; ++k) d += __ldcg(peer_sv[k] + i) - base;
+    delta[i] = d;
+    a += (double)base * (double)d;
+    b += (double)d * (double)d;
+  }
+  block_sum_atomic<kT>(a, acc + 3);
+  block_sum_atomic<kT>(b, acc + 4);
+}
+
+// Fused axpy + all-gather: v = sv₀ + γΔ on shard [lo, hi), written into every worker's sv and sv₀.
+__global__ void k_agg_apply(float *const *peer_sv, float *const *peer_sv0, int K, const float *sv0, const float *delta,
+                            int64_t lo, int64_t hi, const double *acc) {
+  const float g = (float)acc[8];
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = sv0[i] + g * delta[i];
+    for (int k = 0; k < K; ++k) {
+      __stcg(peer_sv[k] + i, v);
+      __stcg(peer_sv0[k] + i, v);
+    }
+  }
+  __threadfence_system();  // peer stores visible to the other GPUs before the next collective
+}
+
 __global__ void k_apply_model(float *x, float *x0, int64_t n, const double *acc) {
   const float g = (float)acc[8];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -96,7 +138,112 @@ __global__ void k_apply_model(float *x, float *x0, int64_t n, const double *acc)
 
 }  // namespace
 
+// Peer tables for the fused exchange across processes (world > 1): CUDA IPC handles of every
+// rank's sv allocation (+ the offset of sv in it) and sv₀, exchanged with one ncclAllGather, opened
+// with peer access.  Any failure leaves the NCCL path in place.
+namespace {
+struct IpcRec {
+  cudaIpcMemHandle_t sv, sv0;
+  int64_t sv_off;
+  int32_t pad[2];
+};
+
+scd_status p2p_setup(scd_ctx *c) {
+  c->p2p_state = -1;
+  const int K = c->opt.world, r = c->opt.rank;
+  IpcRec mine{};
+  if (cudaIpcGetMemHandle(&mine.sv, c->sv_base) != cudaSuccess || cudaIpcGetMemHandle(&mine.sv0, c->sv0) != cudaSuccess) {
+    cudaGetLastError();
+    return SCD_OK;
+  }
+  mine.sv_off = (int64_t)(c->sv - c->sv_base);
+  IpcRec *d_all = nullptr;
+  SCD_CK(c, cudaMalloc((void **)&d_all, sizeof(IpcRec) * (size_t)(K + 1)));
+  SCD_CK(c, cudaMemcpyAsync(d_all + K, &mine, sizeof(IpcRec), cudaMemcpyHostToDevice, c->stream));
+  SCD_NCK(c, ncclAllGather(d_all + K, d_all, sizeof(IpcRec), ncclUint8, c->nccl, c->stream));
+  std::vector<IpcRec> all((size_t)K);
+  SCD_CK(c, cudaMemcpyAsync(all.data(), d_all, sizeof(IpcRec) * (size_t)K, cudaMemcpyDeviceToHost, c->stream));
+  SCD_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_all);
+  std::vector<float *> ptrs(2 * (size_t)K, nullptr);
+  bool ok = true;
+  for (int k = 0; k < K && ok; ++k) {
+    if (k == r) {
+      ptrs[(size_t)k] = c->sv;
+      ptrs[(size_t)K + k] = c->sv0;
+      continue;
+    }
+    void *a = nullptr, *b = nullptr;
+    ok = cudaIpcOpenMemHandle(&a, all[(size_t)k].sv, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
+         cudaIpcOpenMemHandle(&b, all[(size_t)k].sv0, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    if (a) c->p2p_open.push_back(a);
+    if (b) c->p2p_open.push_back(b);
+    if (ok) {
+      ptrs[(size_t)k] = reinterpret_cast<float *>(a) + all[(size_t)k].sv_off;
+      ptrs[(size_t)K + k] = reinterpret_cast<float *>(b);
+    }
+  }
+  // every rank must succeed, or all use the NCCL path
+  int32_t *d_ok = nullptr;
+  int32_t h_ok = ok ? 1 : 0;
+  SCD_CK(c, cudaMalloc((void **)&d_ok, sizeof(int32_t)));
+  SCD_CK(c, cudaMemcpyAsync(d_ok, &h_ok, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  SCD_NCK(c, ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->nccl, c->stream));
+  SCD_CK(c, cudaMemcpyAsync(&h_ok, d_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  SCD_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_ok);
+  if (!h_ok) {
+    cudaGetLastError();
+    for (void *p : c->p2p_open) cudaIpcCloseMemHandle(p);
+    c->p2p_open.clear();
+    return SCD_OK;
+  }
+  SCD_CK(c, cudaMalloc((void **)&c->p2p_ptrs, sizeof(float *) * 2 * (size_t)K));
+  SCD_CK(c, cudaMemcpy(c->p2p_ptrs, ptrs.data(), sizeof(float *) * 2 * (size_t)K, cudaMemcpyHostToDevice));
+  c->p2p_state = 1;
+  return SCD_OK;
+}
+}  // namespace
+
+// world > 1, fused exchange over peer memory (SCD_P2P_AGG=1).  Barriers are the scalar collectives:
+// (1) all-reduce of the model scalars — every rank's epoch is done before any rank reads its sv;
+// (2) all-reduce of the shard dots — every shard's Δ is formed before any rank overwrites sv/sv₀;
+// (3) a one-word all-reduce — every rank's stores into this rank's sv/sv₀ are complete before its
+// next epoch.
+static scd_status aggregate_p2p(scd_ctx *c, scd_agg mode, double *gamma) {
+  cudaStream_t s = c->stream;
+  const int dual = c->form == SCD_DUAL;
+  const int64_t ns = c->n_shared, nc = c->n_coord;
+  const int K = c->opt.world, r = c->opt.rank;
+  const int64_t lo = ns * r / K, hi = ns * (r + 1) / K;
+  float **peer = c->p2p_ptrs;
+  SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 16, s));
+  k_model_dots<<<grid_for(nc, kT), kT, 0, s>>>(c->x, c->x0, c->y, nc, dual, c->acc);
+  SCD_NCK(c, ncclAllReduce(c->acc, c->acc, 3, ncclDouble, ncclSum, c->nccl, s));
+  k_agg_reduce<<<grid_for(hi - lo, kT), kT, 0, s>>>(peer, K, c->sv0, lo, hi, c->comm, c->acc);
+  SCD_NCK(c, ncclAllReduce(c->acc + 3, c->acc + 3, 2, ncclDouble, ncclSum, c->nccl, s));
+  k_gamma<<<1, 1, 0, s>>>(c->acc, (int)mode, (int)c->form, (double)K, c->lam, (double)c->n_global);
+  k_agg_apply<<<grid_for(hi - lo, kT), kT, 0, s>>>(peer, peer + K, K, c->sv0, c->comm, lo, hi, c->acc);
+  SCD_NCK(c, ncclAllReduce(c->acc + 9, c->acc + 9, 1, ncclDouble, ncclSum, c->nccl, s));
+  k_apply_model<<<grid_for(nc, kT), kT, 0, s>>>(c->x, c->x0, nc, c->acc);
+  SCD_CKL(c, "aggregate (fused peer exchange)");
+  c->launches += 5;
+  double g = 0.0;
+  SCD_CK(c, cudaMemcpyAsync(&g, c->acc + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SCD_CK(c, cudaStreamSynchronize(s));
+  if (gamma) *gamma = g;
+  return SCD_OK;
+}
+
 scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
+  // (a 1-rank communicator runs the same fused path: IPC export, handle all-gather, barriers)
+  if (c->nccl && getenv("SCD_P2P_AGG") && atoi(getenv("SCD_P2P_AGG")) == 1) {
+    if (c->p2p_state == 0) {
+      scd_status st = p2p_setup(c);
+      if (st != SCD_OK) return st;
+    }
+    if (c->p2p_state == 1) return aggregate_p2p(c, mode, gamma);
+  }
   cudaStream_t s = c->stream;
   const int dual = c->form == SCD_DUAL;
   const int64_t ns = c->n_shared, nc = c->n_coord;
@@ -125,29 +272,39 @@ scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
   return SCD_OK;
 }
 
-// k logical workers on one device: the "all-reduce" is a device-side sum into ctx[0]'s buffers.
+// k logical workers on one device: the fused peer-memory kernels with the k contexts as the peers
+// and one shard (the whole vector).
 scd_status aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, double *gamma) {
   scd_ctx *c0 = cs[0];
   for (int i = 0; i < k; ++i) SCD_CK(cs[i], cudaStreamSynchronize(cs[i]->stream));
   cudaStream_t s = c0->stream;
   const int dual = c0->form == SCD_DUAL;
   const int64_t ns = c0->n_shared;
+  std::vector<float *> ptrs(2 * (size_t)k);
+  for (int i = 0; i < k; ++i) {
+    ptrs[(size_t)i] = cs[i]->sv;
+    ptrs[(size_t)k + i] = cs[i]->sv0;
+  }
+  float **d_ptrs = nullptr;
+  SCD_CK(c0, cudaMallocAsync((void **)&d_ptrs, sizeof(float *) * 2 * (size_t)k, s));
+  SCD_CK(c0, cudaMemcpyAsync(d_ptrs, ptrs.data(), sizeof(float *) * 2 * (size_t)k, cudaMemcpyHostToDevice, s));
   SCD_CK(c0, cudaMemsetAsync(c0->acc, 0, sizeof(double) * 16, s));
   for (int i = 0; i < k; ++i) {
     scd_ctx *c = cs[i];
     k_model_dots<<<grid_for(c->n_coord, kT), kT, 0, s>>>(c->x, c->x0, c->y, c->n_coord, dual, c0->acc);
-    k_delta<<<grid_for(ns, kT), kT, 0, s>>>(c->sv, c->sv0, ns, i == 0, c0->comm);
-    c->launches += 2;
+    c->launches += 1;
   }
-  k_shared_dots<<<grid_for(ns, kT), kT, 0, s>>>(c0->sv0, c0->comm, ns, c0->acc);
+  k_agg_reduce<<<grid_for(ns, kT), kT, 0, s>>>(d_ptrs, k, c0->sv0, 0, ns, c0->comm, c0->acc);
   k_gamma<<<1, 1, 0, s>>>(c0->acc, (int)mode, (int)c0->form, (double)k, c0->lam, (double)c0->n_global);
+  k_agg_apply<<<grid_for(ns, kT), kT, 0, s>>>(d_ptrs, d_ptrs + k, k, c0->sv0, c0->comm, 0, ns, c0->acc);
+  c0->launches += 3;
   for (int i = 0; i < k; ++i) {
     scd_ctx *c = cs[i];
-    k_apply_shared<<<grid_for(ns, kT), kT, 0, s>>>(c->sv, c->sv0, c0->comm, ns, c0->acc);
     k_apply_model<<<grid_for(c->n_coord, kT), kT, 0, s>>>(c->x, c->x0, c->n_coord, c0->acc);
-    c->launches += 2;
+    c->launches += 1;
   }
   SCD_CKL(c0, "aggregate_group kernels");
+  cudaFreeAsync(d_ptrs, s);
   double g = 0.0;
   SCD_CK(c0, cudaMemcpyAsync(&g, c0->acc + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
   SCD_CK(c0, cudaStreamSynchronize(s));

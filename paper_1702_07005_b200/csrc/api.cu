@@ -66,6 +66,8 @@ void free_ctx(scd_ctx *c) {
   cudaFree(c->acc);
   cudaFree(c->vec64);
   cudaFree(c->comm);
+  for (void *p : c->p2p_open) cudaIpcCloseMemHandle(p);
+  cudaFree(c->p2p_ptrs);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto &p : c->ev_pending) {
     cudaEventDestroy(p.second.first);

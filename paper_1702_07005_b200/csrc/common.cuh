@@ -141,6 +141,9 @@ struct scd_ctx {
   double *vec64 = nullptr;  // [n_shared] fp64 (u = Aβ or v = Aᵀα)
   float *comm = nullptr;    // [n_shared] fp32 aggregation buffer (Δ of the shared vector)
   ncclComm_t nccl = nullptr;
+  int p2p_state = 0;                  // fused peer-memory aggregation: 0 = not set up, 1 = ready, -1 = unavailable
+  float **p2p_ptrs = nullptr;         // device [2 * world]: every rank's sv, then every rank's sv0
+  std::vector<void *> p2p_open;       // IPC mappings to close at destroy
   // profiling
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;

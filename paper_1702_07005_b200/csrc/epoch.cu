@@ -1211,6 +1211,11 @@ void *cluster_kernel(int cl) {
   switch (cl) {
     case 2: return (void *)k_epoch_cluster<FORM, 2, kClusterThreads, kClE, WILD>;
     case 4: return (void *)k_epoch_cluster<FORM, 4, kClusterThreads, kClE, WILD>;
+    case 16: {  // non-portable cluster size: opt in once per instantiation
+      void *fn = (void *)k_epoch_cluster<FORM, 16, kClusterThreads, kClE, WILD>;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      return fn;
+    }
     default: return (void *)k_epoch_cluster<FORM, 8, kClusterThreads, kClE, WILD>;
   }
 }
@@ -1331,7 +1336,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
     // cluster size: large clusters split one very long coordinate over more SMs, small ones keep
     // more coordinates in flight; SCD_CLUSTER = 2|4|8 overrides
     static const int env_cl = getenv("SCD_CLUSTER") ? atoi(getenv("SCD_CLUSTER")) : 0;
-    b.cl = (env_cl == 2 || env_cl == 4 || env_cl == 8) ? env_cl : kClusterCtas;
+    b.cl = (env_cl == 2 || env_cl == 4 || env_cl == 8 || env_cl == 16) ? env_cl : kClusterCtas;
   }
   if (b.hot > 0 && (b.lanes != 8 || c->opt.wild)) b.hot = 0;
   if (b.hot > 0) {

@@ -368,3 +368,26 @@ def test_sub_epoch_aggregation_matches_oracle(form):
     for k, s in enumerate(solvers):
         x[owner == k] = s.get_model()
     assert _rel(x, xo) <= 1e-4
+
+
+@pytest.mark.parametrize("form", ["dual", "primal"])
+def test_fused_peer_aggregation_single_rank(c2s, form, monkeypatch):
+    """The fused peer-memory exchange (SCD_P2P_AGG=1: IPC export and handle all-gather, fused
+    reduce-scatter + dots, fused axpy + all-gather, the three scalar-collective barriers) with a
+    1-rank communicator must equal the communicator-free result (same γ to fp64 rounding of the
+    same sums, identical model)."""
+    monkeypatch.setenv("SCD_P2P_AGG", "1")
+    d, pr = c2s
+    uid = scd.nccl_unique_id()
+    comm = scd.nccl_comm_init(uid, 1, 0)
+    args = (d["ptr"], d["idx"], d["val"]) if form == "dual" else (pr.cptr, pr.cidx, pr.cval)
+    a = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=3, deterministic=True, nccl_comm=comm)
+    b = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=3, deterministic=True)
+    for t in (1, 2, 3):
+        a.epoch(t)
+        b.epoch(t)
+        assert a.aggregate("optimal") == pytest.approx(b.aggregate("optimal"), rel=1e-12)
+    assert np.array_equal(a.get_model(), b.get_model())
+    np.testing.assert_array_equal(a.get_shared(), b.get_shared())
+    a.close()
+    scd.nccl_comm_destroy(comm)
