@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, form, mode, out):
+def _worker(rank, world, port, form, mode, out, protocol="allreduce"):
     import torch
     import torch.distributed as dist
 
@@ -50,13 +50,26 @@ def _worker(rank, world, port, form, mode, out):
             else:
                 solver.dual_epoch(pr, xk, sk, order, nrm, n_global=pr.N)
             dx = (xk - x0)[loc]
-            delta = torch.from_numpy(sk - s0)
             yk = pr.y[loc] if form == "dual" else np.zeros(len(loc))
             scal = torch.tensor([x0[loc] @ dx, dx @ dx, yk @ dx], dtype=torch.float64)
-            dist.all_reduce(delta)  # Σ_k Δsv_k
-            dist.all_reduce(scal)   # Σ_k scalars (disjoint supports)
-            delta = delta.numpy()
-            a_sd, a_dd = s0 @ delta, delta @ delta  # replicated vectors: not reduced
+            if protocol == "allreduce":  # NCCL path of scd_aggregate
+                delta = torch.from_numpy(sk - s0)
+                dist.all_reduce(delta)  # Σ_k Δsv_k
+                dist.all_reduce(scal)   # Σ_k scalars (disjoint supports)
+                delta = delta.numpy()
+                a_sd, a_dd = s0 @ delta, delta @ delta  # replicated vectors: not reduced
+            else:  # fused peer-memory path (aggregate.cu k_agg_reduce / k_agg_apply): own shard only
+                n = len(s0)
+                lo, hi = n * rank // K, n * (rank + 1) // K
+                peers = [torch.zeros(n, dtype=torch.float64) for _ in range(K)]
+                dist.all_gather(peers, torch.from_numpy(sk))  # the peer reads of every rank's sv
+                d_sh = sum(p.numpy()[lo:hi] - s0[lo:hi] for p in peers)
+                scal = torch.cat([scal, torch.tensor([s0[lo:hi] @ d_sh, d_sh @ d_sh], dtype=torch.float64)])
+                dist.all_reduce(scal)  # model scalars + shard dots: the second barrier
+                a_sd, a_dd = float(scal[3]), float(scal[4])
+                shards = [torch.zeros(n * (k + 1) // K - n * k // K, dtype=torch.float64) for k in range(K)]
+                dist.all_gather(shards, torch.from_numpy(d_sh))  # k_agg_apply's stores of every shard
+                delta = torch.cat(shards).numpy()
             lamN = pr.lam * pr.N
             if mode == "average":
                 g = 1.0 / K
@@ -96,15 +109,17 @@ def _worker(rank, world, port, form, mode, out):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("protocol", ["allreduce", "sharded"])
 @pytest.mark.parametrize("form", ["dual", "primal"])
 @pytest.mark.parametrize("mode", ["optimal", "average"])
-def test_two_process_aggregation_matches_simulator(form, mode):
+def test_two_process_aggregation_matches_simulator(form, mode, protocol):
+    """Both exchange protocols of scd_aggregate (NCCL all-reduce; fused sharded peer exchange)."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, form, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, form, mode, q, protocol)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
