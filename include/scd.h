@@ -207,6 +207,8 @@ scd_status scd_profile_read(scd_ctx *c, double *ms_out, int64_t *count_out, int3
 const char *scd_last_error(const scd_ctx *c);   /* context-owned, valid until the next call on c */
 const char *scd_last_global_error(void);         /* thread-local, for context-free calls */
 const char *scd_status_string(scd_status s);
+/* ABI check for bindings: sizes_out[0..2] = sizeof(scd_matrix), sizeof(scd_options), sizeof(scd_info). */
+void scd_struct_sizes(int64_t *sizes_out);
 void scd_destroy(scd_ctx *c);                    /* NULL-safe; syncs the stream; frees owned memory */
 
 /* ---- integer artefacts (computed on the device; bit-exact with the oracle) ---- */

@@ -94,6 +94,13 @@ void scd_default_options(scd_options *o) {
   o->validate = 1;
 }
 
+void scd_struct_sizes(int64_t *sizes_out) {
+  if (!sizes_out) return;
+  sizes_out[0] = (int64_t)sizeof(scd_matrix);
+  sizes_out[1] = (int64_t)sizeof(scd_options);
+  sizes_out[2] = (int64_t)sizeof(scd_info);
+}
+
 const char *scd_status_string(scd_status s) {
   switch (s) {
     case SCD_OK: return "SCD_OK";

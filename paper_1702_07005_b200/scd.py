@@ -56,7 +56,7 @@ _lib = None
 EXPORTS = ("scd_default_options", "scd_create", "scd_epoch", "scd_epoch_part", "scd_objective", "scd_duality_gap", "scd_aggregate",
            "scd_aggregate_group", "scd_evaluate_group", "scd_get_model", "scd_get_shared", "scd_set_model", "scd_recompute_shared",
            "scd_get_stream", "scd_get_info", "scd_profile_read", "scd_last_error", "scd_last_global_error",
-           "scd_status_string", "scd_destroy", "scd_permutation", "scd_partition", "scd_transpose",
+           "scd_status_string", "scd_struct_sizes", "scd_destroy", "scd_permutation", "scd_partition", "scd_transpose",
            "scd_nccl_unique_id", "scd_nccl_comm_init", "scd_nccl_comm_destroy")
 
 
@@ -88,6 +88,7 @@ def lib():
             "scd_last_error": (C.c_char_p, [V]),
             "scd_last_global_error": (C.c_char_p, []),
             "scd_status_string": (C.c_char_p, [C.c_int]),
+            "scd_struct_sizes": (None, [P]),
             "scd_destroy": (None, [V]),
             "scd_permutation": (C.c_int, [C.c_uint64, U32, U32, I64, P]),
             "scd_partition": (C.c_int, [C.c_uint64, I64, I32, P]),

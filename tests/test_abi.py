@@ -47,6 +47,17 @@ def test_invalid_arguments_rejected_before_any_device_work():
     assert e.value.status == 1
 
 
+def test_binding_structs_match_the_header():
+    """The ctypes mirrors of scd_matrix / scd_options / scd_info have the C sizes (a field added to
+    the header but not to the binding would corrupt memory)."""
+    import paper_1702_07005_b200 as p
+    from paper_1702_07005_b200 import scd as b
+
+    out = (ctypes.c_int64 * 3)()
+    p.lib().scd_struct_sizes(out)
+    assert list(out) == [ctypes.sizeof(b.Matrix), ctypes.sizeof(b.Options), ctypes.sizeof(b.Info)]
+
+
 def test_status_strings():
     import paper_1702_07005_b200 as p
 
