@@ -896,7 +896,7 @@ struct HotArgs {
 };
 
 template <int FORM, int G, int E, bool VIEW>
-__global__ void __launch_bounds__(256) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
+__global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
   constexpr int CPW = 32 / G;
   const unsigned FULL = 0xffffffffu;
   extern __shared__ float4 s_dyn[];
@@ -1289,23 +1289,27 @@ int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t
   return (int64_t)((budget / (double)inflight - 1.0) / (double)k);
 }
 
-// Hot-set bin (k_epoch_group_hot): 256-thread CTAs, 32 rows in flight per CTA, window F batches.
-// The grid is lowered (in steps of one CTA per SM, not below two per SM) until F >= 6 fits the
-// budget: longer windows combine more and beat extra CTAs (profiles/hot_sweep_r1.txt).
-// SCD_HOT_F / SCD_HOT_CTAS (CTAs per SM) override (experiments).
+// Hot-set bin (k_epoch_group_hot): 512-thread CTAs (64 rows in flight per CTA, one CTA per SM),
+// window F batches.  At a fixed budget the rows a CTA combines per flush (rows per CTA x F) is what
+// counts: 512 threads at F = 7 beat 256 threads at F = 7 with twice the CTAs (26.9 vs 31.9 ms on a
+// C5 shard).  The grid is lowered (in steps of one CTA per SM, not below one per SM) until F >= 6
+// fits the budget.  SCD_HOT_T=256, SCD_HOT_F, SCD_HOT_CTAS (CTAs per SM) override (experiments).
 void hot_launch_shape(scd_ctx *c, Bin &b) {
   void *fn = bin_kernel(c, b);
   const size_t smem = 8 * (size_t)b.hot;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem);
+  const int T0 = getenv("SCD_HOT_T") && atoi(getenv("SCD_HOT_T")) == 256 ? 256 : 512;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T0, smem);
   if (occ < 1) occ = 1;
   if (const char *e = getenv("SCD_HOT_CTAS")) occ = std::max(1, std::min(occ, atoi(e)));
-  const int64_t k = c->hot_view ? 2 : 1, rows = 256 / 8;
+  const int T = getenv("SCD_HOT_T") && atoi(getenv("SCD_HOT_T")) == 256 ? 256 : 512;
+  const int64_t k = c->hot_view ? 2 : 1, rows = T / 8;
   const int64_t need = (b.count + rows - 1) / rows;
   int64_t grid = std::min<int64_t>((int64_t)c->nsm * occ, std::max<int64_t>(need, 1));
   const char *fe = getenv("SCD_HOT_F");
-  while (!fe && combine_window(c, b, grid * rows, k) < 6 && grid > 2 * (int64_t)c->nsm) grid -= c->nsm;
+  const int64_t min_grid = (int64_t)c->nsm * (T == 512 ? 1 : 2);
+  while (!fe && combine_window(c, b, grid * rows, k) < 6 && grid > min_grid) grid -= c->nsm;
   int64_t F = std::max<int64_t>(1, std::min<int64_t>(64, combine_window(c, b, grid * rows, k)));
   if (fe) F = std::max(1, atoi(fe));
   if (!fe && F < 4) {  // too short a window to beat the CTA-combining kernel: use that instead
@@ -1314,7 +1318,7 @@ void hot_launch_shape(scd_ctx *c, Bin &b) {
     return;
   }
   b.grid = (int)std::max<int64_t>(grid, 1);
-  b.block = 256;
+  b.block = T;
   b.flush = (int)F;
 }
 
