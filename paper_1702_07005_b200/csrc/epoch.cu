@@ -1188,6 +1188,7 @@ void *kernel_for(int lanes, int plain) {
     default: {
       // register-resident kernel by default (measured equal-or-faster and half the coordinates in
       // flight); SCD_CTA_KERNEL=stream selects the two-pass streaming variant
+      // read once per process (the launch shape at create and every launch must agree)
       static const bool stream = getenv("SCD_CTA_KERNEL") && std::string(getenv("SCD_CTA_KERNEL")) == "stream";
       return stream ? (void *)k_epoch_stream<FORM, kCtaT, kStreamU, 8> : (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
     }
@@ -1282,7 +1283,7 @@ cudaEvent_t get_event(scd_ctx *c) {
 // gap 15x behind the sequential one after 4 epochs, so the deferred total is also kept <= 1/8 of the
 // bin's coordinates (never binding on the full-size configs).
 int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t k) {
-  static const double frac = getenv("SCD_COMBINE_BUDGET") ? atof(getenv("SCD_COMBINE_BUDGET")) : 1.0;
+  const double frac = getenv("SCD_COMBINE_BUDGET") ? atof(getenv("SCD_COMBINE_BUDGET")) : 1.0;
   double budget = c->opt.max_inflight > 0 ? (double)b.cap : frac * b.tau;
   budget = std::min(budget, (double)b.count / 8.0);
   if (inflight < 1 || budget <= 0) return 0;
@@ -1339,7 +1340,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   if (b.lanes == kLanesCluster) {
     // cluster size: large clusters split one very long coordinate over more SMs, small ones keep
     // more coordinates in flight; SCD_CLUSTER = 2|4|8 overrides
-    static const int env_cl = getenv("SCD_CLUSTER") ? atoi(getenv("SCD_CLUSTER")) : 0;
+    const int env_cl = getenv("SCD_CLUSTER") ? atoi(getenv("SCD_CLUSTER")) : 0;
     b.cl = (env_cl == 2 || env_cl == 4 || env_cl == 8 || env_cl == 16) ? env_cl : kClusterCtas;
   }
   if (b.hot > 0 && (b.lanes != 8 || c->opt.wild)) b.hot = 0;
