@@ -221,6 +221,26 @@ scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_
  * Within each output outer index, entries appear in increasing input-outer order.
  * If in->val is NULL (implicit values) only the pattern is transposed and val_out is ignored.  */
 scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out, scd_mem out_mem);
+/* Renumbering of the inner index space by frequency (the "renumber by frequency at load" of the
+ * data layer, SURVEY K8'): new id of inner index j = its rank by (number of stored entries with index
+ * j, descending; j ascending).  Output: the same offsets (ptr_out[outer+1]), the relabelled entries
+ * re-sorted increasingly within each outer index (idx_out/val_out[nnz], values moved with their
+ * entries), and new_of_old_out[inner] (caller-allocated, in out_mem) so a shared vector computed on
+ * the renumbered matrix maps back as x_old[j] = x_new[new_of_old[j]].  Computed on the device; integer
+ * results are exact.  The head-combining epoch kernel needs frequency-ranked indices.
+ * Errors: SCD_E_INVALID_ARG (NULL / bad shape / inner > INT32_MAX), SCD_E_OOM, SCD_E_CUDA.          */
+scd_status scd_renumber(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out,
+                        int32_t *new_of_old_out, scd_mem out_mem);
+
+/* ---- LIBSVM reader (host; the paper's datasets, P:254 webspam, P:460 criteo) ----
+ * Format: one example per line, `label index:value ...`, 1-based strictly increasing indices per
+ * line; text after '#' is a comment; blank lines are skipped; values parsed as double and rounded to
+ * fp32; indices become 0-based.  n_cols_hint > 0 fixes the number of columns (error if an index
+ * exceeds it), else n_cols = largest index.  Two passes: scd_libsvm_size reports the shape, then
+ * scd_libsvm_read fills caller-allocated host CSR arrays ptr[n_rows+1], idx[nnz], val[nnz],
+ * y[n_rows].  Errors: SCD_E_INVALID_ARG with the file / line in scd_last_global_error().          */
+scd_status scd_libsvm_size(const char *path, int64_t n_cols_hint, int64_t *n_rows, int64_t *nnz, int64_t *n_cols);
+scd_status scd_libsvm_read(const char *path, int64_t n_cols_hint, int64_t *ptr, int32_t *idx, float *val, float *y);
 
 /* ---- NCCL bootstrap helpers (the caller broadcasts the 128-byte id, e.g. via torch.distributed) ---- */
 scd_status scd_nccl_unique_id(void *id_out_128);

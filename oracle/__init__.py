@@ -10,11 +10,12 @@ Modules:
               distributed Alg. 3/4 simulator
   ``_lib``    ctypes loader for ``liboracle.so`` (Feistel permutation, partition, transpose,
               norms, epochs)
+  ``data``    data-layer references: frequency renumbering of the inner indices, LIBSVM parsing
 
 Pinned by tests/test_oracle_pins.py against what the paper and mathematics fix (closed-form
 normal equations, stationarity, monotone objective, strong duality, exact line search, SPEC
 hand values).  Parity unpinned (no paper values; invariants only): the permutation, partition
 and transpose artefacts — see DESIGN.md §5.
 """
-from . import ridge, solver  # noqa: F401
+from . import data, ridge, solver  # noqa: F401
 from ._lib import permutation, partition, transpose, sq_norms, perm_at  # noqa: F401

@@ -85,6 +85,79 @@ void free_ctx(scd_ctx *c) {
 
 }  // namespace
 
+namespace {
+// Matrix-to-matrix utilities (transpose, renumber): stage host inputs / outputs through device
+// buffers and run `op(p, i, v, outer, inner, nnz, dp, di, dv, s, err)` on device pointers.
+// out_outer = outer length of the output (inner for the transpose, outer for the renumbering).
+template <typename Op>
+scd_status matrix_op(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out, scd_mem out_mem,
+                     bool transpose_shape, Op op) {
+  if (!in || !ptr_out || !in->ptr || (in->nnz > 0 && (!idx_out || !in->idx || (in->val && !val_out))))
+    return fail(nullptr, SCD_E_INVALID_ARG, "NULL argument");
+  const bool has_val = in->val != nullptr;
+  const int64_t outer = in->layout == SCD_CSR ? in->n_rows : in->n_cols;
+  const int64_t inner = in->layout == SCD_CSR ? in->n_cols : in->n_rows;
+  if (outer < 0 || inner < 1 || in->nnz < 0) return fail(nullptr, SCD_E_INVALID_ARG, "bad shape");
+  const int64_t nnz = in->nnz, out_outer = transpose_shape ? inner : outer;
+  cudaStream_t s = 0;
+  std::string err;
+  const int64_t *p = in->ptr;
+  const int32_t *i = in->idx;
+  const float *v = in->val;
+  void *tp = nullptr, *ti = nullptr, *tv = nullptr, *op_ = nullptr, *oi = nullptr, *ov = nullptr;
+  scd_status st = SCD_OK;
+  auto alloc = [&](void **q, size_t b) {
+    if (st != SCD_OK) return;
+    if (cudaMalloc(q, b > 0 ? b : 1) != cudaSuccess) st = fail(nullptr, SCD_E_OOM, "matrix op alloc");
+  };
+  if (in->mem == SCD_MEM_HOST) {
+    alloc(&tp, sizeof(int64_t) * (size_t)(outer + 1));
+    alloc(&ti, sizeof(int32_t) * (size_t)nnz);
+    if (has_val) alloc(&tv, sizeof(float) * (size_t)nnz);
+    if (st == SCD_OK) {
+      cudaMemcpy(tp, p, sizeof(int64_t) * (size_t)(outer + 1), cudaMemcpyHostToDevice);
+      if (nnz) {
+        cudaMemcpy(ti, i, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice);
+        if (has_val) cudaMemcpy(tv, v, sizeof(float) * (size_t)nnz, cudaMemcpyHostToDevice);
+      }
+      p = (const int64_t *)tp;
+      i = (const int32_t *)ti;
+      v = (const float *)tv;
+    }
+  }
+  int64_t *dp = ptr_out;
+  int32_t *di = idx_out;
+  float *dv = has_val ? val_out : nullptr;
+  if (out_mem == SCD_MEM_HOST) {
+    alloc(&op_, sizeof(int64_t) * (size_t)(out_outer + 1));
+    alloc(&oi, sizeof(int32_t) * (size_t)nnz);
+    if (has_val) alloc(&ov, sizeof(float) * (size_t)nnz);
+    dp = (int64_t *)op_;
+    di = (int32_t *)oi;
+    dv = (float *)ov;
+  }
+  if (st == SCD_OK) {
+    st = op(p, i, v, outer, inner, nnz, dp, di, dv, s, err);
+    if (st != SCD_OK) fail(nullptr, st, err);
+  }
+  if (st == SCD_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(nullptr, SCD_E_CUDA, "matrix op sync");
+  if (st == SCD_OK && out_mem == SCD_MEM_HOST) {
+    cudaMemcpy(ptr_out, op_, sizeof(int64_t) * (size_t)(out_outer + 1), cudaMemcpyDeviceToHost);
+    if (nnz) {
+      cudaMemcpy(idx_out, oi, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDeviceToHost);
+      if (has_val) cudaMemcpy(val_out, ov, sizeof(float) * (size_t)nnz, cudaMemcpyDeviceToHost);
+    }
+  }
+  cudaFree(tp);
+  cudaFree(ti);
+  cudaFree(tv);
+  cudaFree(op_);
+  cudaFree(oi);
+  cudaFree(ov);
+  return st;
+}
+}  // namespace
+
 extern "C" {
 
 void scd_default_options(scd_options *o) {
@@ -474,71 +547,36 @@ scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_
   return st;
 }
 
+
 scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out, scd_mem out_mem) {
   g_err.clear();
   // in->val == NULL (implicit values) transposes the pattern only; val_out is then ignored
-  if (!in || !ptr_out || !in->ptr || (in->nnz > 0 && (!idx_out || !in->idx || (in->val && !val_out))))
-    return fail(nullptr, SCD_E_INVALID_ARG, "NULL argument");
-  const bool has_val = in->val != nullptr;
-  const int64_t outer = in->layout == SCD_CSR ? in->n_rows : in->n_cols;
+  return matrix_op(in, ptr_out, idx_out, val_out, out_mem, true,
+                   [](const int64_t *p, const int32_t *i, const float *v, int64_t outer, int64_t inner, int64_t nnz,
+                      int64_t *dp, int32_t *di, float *dv, cudaStream_t s, std::string &err) {
+                     return transpose_device(p, i, v, outer, inner, nnz, dp, di, dv, s, err);
+                   });
+}
+
+scd_status scd_renumber(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out,
+                        int32_t *new_of_old_out, scd_mem out_mem) {
+  g_err.clear();
+  if (!new_of_old_out) return fail(nullptr, SCD_E_INVALID_ARG, "NULL argument");
+  if (!in) return fail(nullptr, SCD_E_INVALID_ARG, "NULL argument");
   const int64_t inner = in->layout == SCD_CSR ? in->n_cols : in->n_rows;
-  if (outer < 0 || inner < 1 || in->nnz < 0) return fail(nullptr, SCD_E_INVALID_ARG, "bad shape");
-  const int64_t nnz = in->nnz;
-  cudaStream_t s = 0;
-  std::string err;
-  const int64_t *p = in->ptr;
-  const int32_t *i = in->idx;
-  const float *v = in->val;
-  void *tp = nullptr, *ti = nullptr, *tv = nullptr, *op = nullptr, *oi = nullptr, *ov = nullptr;
-  scd_status st = SCD_OK;
-  auto alloc = [&](void **q, size_t b) {
-    if (st != SCD_OK) return;
-    if (cudaMalloc(q, b > 0 ? b : 1) != cudaSuccess) st = fail(nullptr, SCD_E_OOM, "transpose alloc");
-  };
-  if (in->mem == SCD_MEM_HOST) {
-    alloc(&tp, sizeof(int64_t) * (size_t)(outer + 1));
-    alloc(&ti, sizeof(int32_t) * (size_t)nnz);
-    if (has_val) alloc(&tv, sizeof(float) * (size_t)nnz);
-    if (st == SCD_OK) {
-      cudaMemcpy(tp, p, sizeof(int64_t) * (size_t)(outer + 1), cudaMemcpyHostToDevice);
-      if (nnz) {
-        cudaMemcpy(ti, i, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice);
-        if (has_val) cudaMemcpy(tv, v, sizeof(float) * (size_t)nnz, cudaMemcpyHostToDevice);
-      }
-      p = (const int64_t *)tp;
-      i = (const int32_t *)ti;
-      v = (const float *)tv;
-    }
-  }
-  int64_t *dp = ptr_out;
-  int32_t *di = idx_out;
-  float *dv = has_val ? val_out : nullptr;
+  if (inner < 1 || inner > INT32_MAX) return fail(nullptr, SCD_E_INVALID_ARG, "bad inner size");
+  int32_t *d_map = new_of_old_out;
+  if (out_mem == SCD_MEM_HOST && cudaMalloc((void **)&d_map, sizeof(int32_t) * (size_t)inner) != cudaSuccess)
+    return fail(nullptr, SCD_E_OOM, "renumber alloc");
+  scd_status st = matrix_op(in, ptr_out, idx_out, val_out, out_mem, false,
+                            [&](const int64_t *p, const int32_t *i, const float *v, int64_t outer, int64_t inn,
+                                int64_t nnz, int64_t *dp, int32_t *di, float *dv, cudaStream_t s, std::string &err) {
+                              return renumber_device(p, i, v, outer, inn, nnz, dp, di, dv, d_map, s, err);
+                            });
   if (out_mem == SCD_MEM_HOST) {
-    alloc(&op, sizeof(int64_t) * (size_t)(inner + 1));
-    alloc(&oi, sizeof(int32_t) * (size_t)nnz);
-    if (has_val) alloc(&ov, sizeof(float) * (size_t)nnz);
-    dp = (int64_t *)op;
-    di = (int32_t *)oi;
-    dv = (float *)ov;
+    if (st == SCD_OK) cudaMemcpy(new_of_old_out, d_map, sizeof(int32_t) * (size_t)inner, cudaMemcpyDeviceToHost);
+    cudaFree(d_map);
   }
-  if (st == SCD_OK) {
-    st = transpose_device(p, i, v, outer, inner, nnz, dp, di, dv, s, err);
-    if (st != SCD_OK) fail(nullptr, st, err);
-  }
-  if (st == SCD_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(nullptr, SCD_E_CUDA, "transpose sync");
-  if (st == SCD_OK && out_mem == SCD_MEM_HOST) {
-    cudaMemcpy(ptr_out, op, sizeof(int64_t) * (size_t)(inner + 1), cudaMemcpyDeviceToHost);
-    if (nnz) {
-      cudaMemcpy(idx_out, oi, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDeviceToHost);
-      if (has_val) cudaMemcpy(val_out, ov, sizeof(float) * (size_t)nnz, cudaMemcpyDeviceToHost);
-    }
-  }
-  cudaFree(tp);
-  cudaFree(ti);
-  cudaFree(tv);
-  cudaFree(op);
-  cudaFree(oi);
-  cudaFree(ov);
   return st;
 }
 

@@ -204,6 +204,9 @@ scd_status validate_matrix(scd_ctx *c, int64_t outer, int64_t inner);
 scd_status compute_norms(scd_ctx *c);
 scd_status build_schedule(scd_ctx *c);
 scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau);
+scd_status renumber_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
+                           int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, int32_t *new_of_old, cudaStream_t s,
+                           std::string &err);
 scd_status transpose_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
                             int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, cudaStream_t s, std::string &err);
 

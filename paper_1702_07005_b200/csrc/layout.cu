@@ -2,6 +2,7 @@
 // asynchronous coordinate schedule (length bins), and the stable CSR<->CSC transpose.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 
@@ -114,7 +115,84 @@ __global__ void __launch_bounds__(256) k_count_below(const int32_t *idx, int64_t
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
 }
 
+// sort key of inner index j: occurrences descending, then j ascending (a strict total order)
+__global__ void k_rank_keys(const unsigned long long *cnt, int64_t inner, unsigned long long *key) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < inner; j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long c = cnt[j + 1];  // k_count layout: cnt[j + 1] = occurrences of j
+    key[j] = ((0xFFFFFFFFull - (c > 0xFFFFFFFFull ? 0xFFFFFFFFull : c)) << 32) | (unsigned long long)j;
+  }
+}
+__global__ void k_rank_scatter(const unsigned long long *key_sorted, int64_t inner, int32_t *new_of_old) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < inner; r += (int64_t)gridDim.x * blockDim.x)
+    new_of_old[key_sorted[r] & 0xFFFFFFFFull] = (int32_t)r;
+}
+__global__ void k_relabel(const int32_t *idx, int64_t n, const int32_t *new_of_old, int32_t *out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = new_of_old[idx[k]];
+}
+
 }  // namespace
+
+// Renumbering of the inner index space by frequency (SURVEY K8' "feature renumbering by frequency at
+// load"): new id = rank of the index by (occurrences descending, index ascending); entries relabelled
+// and re-sorted within each outer index (keys are distinct within an outer index, so the order is
+// unique).  Output offsets equal the input ones.  Bit-exact (integer work only; values are moved).
+scd_status renumber_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
+                           int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, int32_t *new_of_old, cudaStream_t s,
+                           std::string &err) {
+  auto ck = [&](cudaError_t e, const char *what) {
+    if (e != cudaSuccess) err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaSuccess;
+  };
+  unsigned long long *cnt = nullptr, *key = nullptr, *key_sorted = nullptr;
+  int32_t *tmp_idx = nullptr;
+  float *tmp_val = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_b = 0;
+  bool ok = ck(cudaMallocAsync((void **)&cnt, sizeof(unsigned long long) * (inner + 1), s), "alloc") &&
+            ck(cudaMallocAsync((void **)&key, sizeof(unsigned long long) * inner, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&key_sorted, sizeof(unsigned long long) * inner, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&tmp_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s), "alloc");
+  if (ok && val) ok = ck(cudaMallocAsync((void **)&tmp_val, sizeof(float) * (nnz > 0 ? nnz : 1), s), "alloc");
+  if (ok) {
+    cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (inner + 1), s);
+    if (nnz > 0) k_count<<<grid_for(nnz, 256), 256, 0, s>>>(idx, nnz, cnt);
+    k_rank_keys<<<grid_for(inner, 256), 256, 0, s>>>(cnt, inner, key);
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp_b, key, key_sorted, inner, 0, 64, s);
+    ok = ck(cudaMallocAsync(&tmp, tmp_b, s), "alloc sort tmp") &&
+         ck(cub::DeviceRadixSort::SortKeys(tmp, tmp_b, key, key_sorted, inner, 0, 64, s), "rank sort");
+  }
+  if (ok) {
+    k_rank_scatter<<<grid_for(inner, 256), 256, 0, s>>>(key_sorted, inner, new_of_old);
+    if (tmp) cudaFreeAsync(tmp, s);
+    tmp = nullptr;
+    ok = ck(cudaMemcpyAsync(optr, ptr, sizeof(int64_t) * (outer + 1), cudaMemcpyDeviceToDevice, s), "copy ptr");
+  }
+  if (ok && nnz > 0) {
+    k_relabel<<<grid_for(nnz, 256), 256, 0, s>>>(idx, nnz, new_of_old, tmp_idx);
+    if (val) ok = ck(cudaMemcpyAsync(tmp_val, val, sizeof(float) * nnz, cudaMemcpyDeviceToDevice, s), "copy val");
+    tmp_b = 0;
+    if (ok && val) {
+      cub::DeviceSegmentedSort::SortPairs(nullptr, tmp_b, tmp_idx, oidx, tmp_val, oval, nnz, outer, ptr, ptr + 1, s);
+      ok = ck(cudaMallocAsync(&tmp, tmp_b, s), "alloc seg sort") &&
+           ck(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_b, tmp_idx, oidx, tmp_val, oval, nnz, outer, ptr, ptr + 1, s),
+              "segmented sort");
+    } else if (ok) {
+      cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_b, tmp_idx, oidx, nnz, outer, ptr, ptr + 1, s);
+      ok = ck(cudaMallocAsync(&tmp, tmp_b, s), "alloc seg sort") &&
+           ck(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_b, tmp_idx, oidx, nnz, outer, ptr, ptr + 1, s),
+              "segmented sort");
+    }
+  }
+  ok = ok && ck(cudaGetLastError(), "renumber kernels");
+  if (tmp) cudaFreeAsync(tmp, s);
+  if (cnt) cudaFreeAsync(cnt, s);
+  if (key) cudaFreeAsync(key, s);
+  if (key_sorted) cudaFreeAsync(key_sorted, s);
+  if (tmp_idx) cudaFreeAsync(tmp_idx, s);
+  if (tmp_val) cudaFreeAsync(tmp_val, s);
+  return ok ? SCD_OK : SCD_E_CUDA;
+}
 
 // Head of the shared vector combined in shared memory by the CTA kernel (k_epoch_cta_head,
 // DESIGN.md §6): H = SCD_HEAD floats (default 8192, 0 = off), used when at least 10% of all

@@ -56,7 +56,7 @@ _lib = None
 EXPORTS = ("scd_default_options", "scd_create", "scd_epoch", "scd_epoch_part", "scd_objective", "scd_duality_gap", "scd_aggregate",
            "scd_aggregate_group", "scd_evaluate_group", "scd_get_model", "scd_get_shared", "scd_set_model", "scd_recompute_shared",
            "scd_get_stream", "scd_get_info", "scd_profile_read", "scd_last_error", "scd_last_global_error",
-           "scd_status_string", "scd_struct_sizes", "scd_destroy", "scd_permutation", "scd_partition", "scd_transpose",
+           "scd_status_string", "scd_struct_sizes", "scd_destroy", "scd_permutation", "scd_partition", "scd_transpose", "scd_renumber", "scd_libsvm_size", "scd_libsvm_read",
            "scd_nccl_unique_id", "scd_nccl_comm_init", "scd_nccl_comm_destroy")
 
 
@@ -93,6 +93,9 @@ def lib():
             "scd_permutation": (C.c_int, [C.c_uint64, U32, U32, I64, P]),
             "scd_partition": (C.c_int, [C.c_uint64, I64, I32, P]),
             "scd_transpose": (C.c_int, [C.POINTER(Matrix), P, P, P, C.c_int]),
+            "scd_renumber": (C.c_int, [C.POINTER(Matrix), P, P, P, P, C.c_int]),
+            "scd_libsvm_size": (C.c_int, [C.c_char_p, I64, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
+            "scd_libsvm_read": (C.c_int, [C.c_char_p, I64, P, P, P, P]),
             "scd_nccl_unique_id": (C.c_int, [P]),
             "scd_nccl_comm_init": (C.c_int, [P, I32, I32, C.POINTER(V)]),
             "scd_nccl_comm_destroy": (C.c_int, [V]),
@@ -315,6 +318,49 @@ def transpose(ptr, idx, val, n_rows: int, n_cols: int, layout: str = "csr"):
     ov = np.empty(max(nnz, 1), np.float32)
     _check(lib().scd_transpose(C.byref(m), op.ctypes.data, oi.ctypes.data, ov.ctypes.data, MEM_HOST))
     return op, oi[:nnz], (ov[:nnz] if v is not None else None)
+
+
+def renumber(ptr, idx, val, n_rows: int, n_cols: int, layout: str = "csr"):
+    """Renumber the inner indices by frequency on the device (scd_renumber).  Host inputs -> numpy
+    outputs, CUDA tensors -> CUDA tensors.  Returns (ptr, idx, val, new_of_old)."""
+    p, mp, kp = _buf(ptr, np.int64)
+    i, mi, ki = _buf(idx, np.int32)
+    v, mv, kv = _buf(val, np.float32) if val is not None else (None, mp, None)
+    lay = CSR if layout == "csr" else CSC
+    outer, inner = (n_rows, n_cols) if lay == CSR else (n_cols, n_rows)
+    nnz = int(kp[-1]) if mp == MEM_HOST else int(kp[-1].item())
+    m = Matrix(lay, n_rows, n_cols, nnz, p, i, v, mp)
+    if mp == MEM_DEVICE:
+        import torch
+
+        dev = kp.device
+        op = torch.empty(outer + 1, dtype=torch.int64, device=dev)
+        oi = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        ov = torch.empty(max(nnz, 1), dtype=torch.float32, device=dev)
+        om = torch.empty(inner, dtype=torch.int32, device=dev)
+        _check(lib().scd_renumber(C.byref(m), op.data_ptr(), oi.data_ptr(), ov.data_ptr(), om.data_ptr(), MEM_DEVICE))
+        return op, oi[:nnz], (ov[:nnz] if v is not None else None), om
+    op = np.empty(outer + 1, np.int64)
+    oi = np.empty(max(nnz, 1), np.int32)
+    ov = np.empty(max(nnz, 1), np.float32)
+    om = np.empty(inner, np.int32)
+    _check(lib().scd_renumber(C.byref(m), op.ctypes.data, oi.ctypes.data, ov.ctypes.data, om.ctypes.data, MEM_HOST))
+    return op, oi[:nnz], (ov[:nnz] if v is not None else None), om
+
+
+def load_libsvm(path: str, n_cols: int | None = None) -> dict:
+    """Read a LIBSVM text file into host CSR arrays (scd_libsvm_size + scd_libsvm_read):
+    dict(ptr, idx, val, y, n_rows, n_cols) with 0-based indices."""
+    L = lib()
+    hint = int(n_cols or 0)
+    r, z, c = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(L.scd_libsvm_size(path.encode(), hint, C.byref(r), C.byref(z), C.byref(c)))
+    ptr = np.empty(r.value + 1, np.int64)
+    idx = np.empty(max(z.value, 1), np.int32)
+    val = np.empty(max(z.value, 1), np.float32)
+    y = np.empty(max(r.value, 1), np.float32)
+    _check(L.scd_libsvm_read(path.encode(), hint, ptr.ctypes.data, idx.ctypes.data, val.ctypes.data, y.ctypes.data))
+    return dict(ptr=ptr, idx=idx[:z.value], val=val[:z.value], y=y[:r.value], n_rows=r.value, n_cols=c.value)
 
 
 def nccl_unique_id() -> bytes:
