@@ -1,6 +1,7 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer (memcheck / racecheck):
 deterministic and asynchronous epochs (CTA, sub-warp, combining, cluster bins), the head-combining
-CTA kernel (plain and with the shared-memory view), the die-split kernel, the wild scatter, empty
+CTA kernel (plain and with the shared-memory view), the die-split kernel, the wild scatter, the
+hot-set kernel (and its view), the fused peer-memory aggregation, device renumbering, empty
 rows/cols, implicit values, gap/objective, aggregation (group and 1-rank NCCL), transpose,
 permutation."""
 import os
@@ -77,4 +78,24 @@ for env in ({}, {"SCD_HEAD_SNAP": "1", "SCD_HEAD_FLUSH": "2"}, {"SCD_DIE_SPLIT":
     print("c3 prefix", env, inf["bins"][0], "die_split", inf["die_split"], run(c3, "dual"), flush=True)
     for k in env:
         del os.environ[k]
+# criteo-shaped rows with λN = 2e5 (as in the 8-GPU shards): the hot-set kernel (and its view variant)
+c5h = synth.gen_host(synth.CONFIGS["C5"].with_rows(1_000_000))
+c5h["lam"] = 0.2
+for env in ({}, {"SCD_HOT_VIEW": "1", "SCD_HOT_F": "4"}):
+    os.environ.update(env)
+    s = scd.Solver(c5h["ptr"], c5h["idx"], c5h["val"], c5h["n_rows"], c5h["n_cols"], c5h["y"], c5h["lam"], "dual",
+                   seed=3)
+    inf = s.info()
+    s.close()
+    print("c5 hot", env, inf["bins"][0], run(c5h, "dual"), flush=True)
+    for k in env:
+        del os.environ[k]
+# fused peer-memory aggregation through a 1-rank communicator; device renumbering
+os.environ["SCD_P2P_AGG"] = "1"
+comm = scd.nccl_comm_init(scd.nccl_unique_id(), 1, 0)
+print("p2p", run(e, "dual", nccl_comm=comm), run(e, "primal", nccl_comm=comm), flush=True)
+scd.nccl_comm_destroy(comm)
+del os.environ["SCD_P2P_AGG"]
+r = scd.renumber(e["ptr"], e["idx"], e["val"], 300, 200, "csr")
+print("renumber", int(r[3].sum()), flush=True)
 print("sanitize_small done")
