@@ -151,3 +151,35 @@ def test_hot_set_kernel_criteo_prefix(monkeypatch):
     assert gaps[-1] <= 1e-5
     for t in (0, 1, 3):
         assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
+
+
+def test_hot_set_kernel_ragged_short_rows(monkeypatch):
+    """k_epoch_group_hot with ragged short rows (1..64 entries: every lane/slot validity pattern of
+    the 8 x 8 register tile) over a Zipf(1.1) feature distribution; λN = 4e5 so the window fits.
+    Checked against the oracle's optimum and the sequential band, and against the CTA-combining
+    kernel (SCD_HOT=0) on the same input."""
+    monkeypatch.delenv("SCD_HOT", raising=False)
+    cfg = synth.ZipfRowsCfg("ragged", 400_000, 200_000, 200_000, 1.1, 24.0, 0.8, 1, 64, seed=9)
+    d = synth.gen_host(cfg)
+    pr = solver.Problem.from_csr(d, lam=1.0)
+    _, _, hist = solver.solve(pr, "dual", 6, seed=6)
+    A = pr.A()
+    finals = {}
+    for hot in ("4096", "0"):
+        monkeypatch.setenv("SCD_HOT", hot)
+        s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=6)
+        b = s.info()["bins"][0]
+        assert b["lanes"] == 8 and ((b["hot"] > 0) == (hot != "0")), b
+        gaps = []
+        for t in range(1, 7):
+            s.epoch(t)
+            gaps.append(s.duality_gap())
+        x = s.get_model().astype(np.float64)
+        s.close()
+        print(hot, "gpu gaps", ["%.2e" % g for g in gaps])
+        for t in (0, 2):
+            assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (hot, t, gaps[t], hist[t]["gap"])
+        finals[hot] = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+    print("seq gaps", ["%.2e" % h["gap"] for h in hist])
+    assert abs(finals["4096"] - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
+    assert abs(finals["0"] - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
