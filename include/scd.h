@@ -196,6 +196,10 @@ typedef struct {
   int64_t split_nnz0;     /* die split: stored entries whose shared-vector element is homed on die 0 */
   int32_t bin_hot[4];     /* per bin: > 0 = hot-set kernel with this many hot shared-vector entries (hot.cu) */
   double hot_cover;       /* share of the hot bin's stored entries that fall on a hot entry */
+  int32_t tail_snap;      /* head kernel: 1 = tail gathers (ids >= bin_head) read a copy of the shared vector
+                             refreshed before every slice; 0 = off */
+  double tail_tau;        /* staleness bound of the coupling through the tail entries (coordinates); the
+                             tail copy is used only while a slice's coordinates are <= tail_tau / 2 */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

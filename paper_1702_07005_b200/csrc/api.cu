@@ -50,6 +50,7 @@ void free_ctx(scd_ctx *c) {
   cudaFree(c->x0);
   cudaFree(c->sv_base);
   cudaFree(c->sv0);
+  cudaFree(c->svr);
   cudaFree(c->norm);
   cudaFree(c->empty_list);
   for (int i = 0; i < kMaxBins; ++i) cudaFree(c->bins[i].list);
@@ -481,6 +482,8 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->die_lat[1] = c->die_lat[1];
   info->split_nnz0 = c->split_nnz0;
   info->hot_cover = c->hot_cover;
+  info->tail_snap = c->tail_snap;
+  info->tail_tau = c->tail_tau;
   info->inflight_cap = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i) {
     info->bin_cap[i] = c->bins[i].cap;

@@ -157,6 +157,11 @@ struct scd_ctx {
   bool hot_view = false;              // hot-set kernel also keeps a per-CTA view of the hot values
   double hot_cover = 0.0;             // share of the bin's entries that are hot
   bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)
+  int tail_snap = 0;                  // head kernel reads the tail [tail_lo, tail_hi) of the shared vector from a
+                                      // read copy refreshed before every slice: 1 = L2 loads, 2 = L1-cached loads
+  float *svr = nullptr;               // device [n_shared]: the read copy (only [tail_lo, tail_hi) is maintained)
+  int64_t tail_lo = 0, tail_hi = 0;
+  double tail_tau = 0.0;              // staleness bound of the head bin's coupling through the tail entries
   bool die_split = false;
   uint8_t *sm_die = nullptr;          // device [kMaxSm]: die of each SM id
   int n_die_sm[2] = {0, 0};
@@ -204,6 +209,7 @@ scd_status validate_matrix(scd_ctx *c, int64_t outer, int64_t inner);
 scd_status compute_norms(scd_ctx *c);
 scd_status build_schedule(scd_ctx *c);
 scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau);
+scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, int64_t lo, double *tau);
 scd_status renumber_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
                            int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, int32_t *new_of_old, cudaStream_t s,
                            std::string &err);

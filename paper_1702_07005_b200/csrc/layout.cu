@@ -90,6 +90,28 @@ __global__ void k_abs_scatter(const int64_t *ptr, const int32_t *idx, const floa
     if (lane == 0) atomicAdd(acc + 1, (double)norm[o]);
   }
 }
+// Tail part of the same sum: s[idx[k]] += |val[k]| for idx[k] >= lo only; acc[2] += Σ val² of those
+// entries (their diagonal terms), acc[1] += Σ_bin ||a||² as above
+__global__ void k_abs_scatter_tail(const int64_t *ptr, const int32_t *idx, const float *val, const int32_t *list,
+                                   int64_t count, const float *norm, int32_t lo, double *s, double *acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double sq = 0.0;
+  for (int64_t j = warp; j < count; j += nwarps) {
+    const int64_t o = list ? list[j] : j;
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) {
+      const int32_t i = idx[k];
+      if (i < lo) continue;
+      const double v = (double)val_at(val, k);
+      atomicAdd(s + i, fabs(v));
+      sq += v * v;
+    }
+    if (lane == 0) atomicAdd(acc + 1, (double)norm[o]);
+  }
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0 && sq != 0.0) atomicAdd(acc + 2, sq);
+}
 // acc[0] += Σ s_i²
 __global__ void __launch_bounds__(256) k_sumsq(const double *s, int64_t n, double *acc) {
   double a = 0.0;
@@ -113,6 +135,14 @@ __global__ void __launch_bounds__(256) k_count_below(const int32_t *idx, int64_t
     cnt += __ldcs(idx + i) < H;
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
+}
+
+__global__ void __launch_bounds__(256) k_max_idx(const int32_t *idx, int64_t n, int *out) {
+  int m = -1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, __ldcs(idx + i));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 // sort key of inner index j: occurrences descending, then j ascending (a strict total order)
@@ -216,6 +246,31 @@ static scd_status choose_head(scd_ctx *c, int *head) {
   return SCD_OK;
 }
 
+// Tail read copy of the head kernel: the gathers of tail entries (ids >= H) are served
+// from svr, a copy of sv[H, max id] refreshed before every slice, so the lines that are gathered and
+// the lines that take REDs are disjoint.  SCD_TAIL_SNAP = 1 (L2 loads) | 2 (L1-cached loads) | 0.
+static scd_status setup_tail_snap(scd_ctx *c, int head) {
+  c->tail_snap = 0;
+  const char *e = getenv("SCD_TAIL_SNAP");
+  const int mode = e ? atoi(e) : 1;
+  if (head <= 0 || (mode != 1 && mode != 2) || c->form != SCD_DUAL) return SCD_OK;
+  int *d = nullptr, h = -1;
+  SCD_CK(c, cudaMallocAsync((void **)&d, sizeof(int), c->stream));
+  SCD_CK(c, cudaMemsetAsync(d, 0xff, sizeof(int), c->stream));
+  k_max_idx<<<grid_for(c->nnz, 256, 148 * 8), 256, 0, c->stream>>>(c->idx, c->nnz, d);
+  SCD_CKL(c, "k_max_idx");
+  SCD_CK(c, cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  SCD_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFreeAsync(d, c->stream);
+  if (h < head) return SCD_OK;
+  c->tail_lo = head;
+  c->tail_hi = (int64_t)h + 1;
+  SCD_CK(c, cudaMalloc((void **)&c->svr, sizeof(float) * (size_t)c->n_shared));
+  SCD_CK(c, cudaMemsetAsync(c->svr, 0, sizeof(float) * (size_t)c->n_shared, c->stream));
+  c->tail_snap = mode;
+  return SCD_OK;
+}
+
 // Staleness bound for one bin of the asynchronous schedule.  With τ coordinates of
 // the bin in flight, a coordinate's update misses up to τ-1 concurrent updates.  Treating them as
 // one block-Jacobi step, the step stays contractive while τ·c̄ < λN + d̄ (diagonal dominance of the
@@ -236,6 +291,28 @@ scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, do
   SCD_CK(c, cudaStreamSynchronize(s));
   const double n = (double)(count > 1 ? count : 2);
   const double cbar = (h[0] - h[1]) / (n * (n - 1.0));
+  const double dbar = h[1] / n + c->lamN;
+  *tau = cbar > 0 ? dbar / cbar : 1e18;
+  return SCD_OK;
+}
+
+// Staleness bound of the bin's coupling through the shared-vector entries >= lo only (the tail read
+// copy of the head kernel): τ_tail = (λN + d̄) / c̄_tail, c̄_tail from ||(|A_b[:, lo:]|ᵀ1)||²
+// minus its diagonal terms.
+scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, int64_t lo, double *tau) {
+  cudaStream_t s = c->stream;
+  double *vec = c->vec64;
+  SCD_CK(c, cudaMemsetAsync(vec, 0, sizeof(double) * (size_t)c->n_shared, s));
+  SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 3, s));
+  k_abs_scatter_tail<<<grid_for(count * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, d_list, count, c->norm,
+                                                                         (int32_t)lo, vec, c->acc);
+  k_sumsq<<<grid_for(c->n_shared - lo, 256, 148 * 8), 256, 0, s>>>(vec + lo, c->n_shared - lo, c->acc);
+  SCD_CKL(c, "tail coupling estimate");
+  double h[3];
+  SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SCD_CK(c, cudaStreamSynchronize(s));
+  const double n = (double)(count > 1 ? count : 2);
+  const double cbar = (h[0] - h[2]) / (n * (n - 1.0));
   const double dbar = h[1] / n + c->lamN;
   *tau = cbar > 0 ? dbar / cbar : 1e18;
   return SCD_OK;
@@ -302,6 +379,7 @@ scd_status build_schedule(scd_ctx *c) {
   int head = 0;
   if (scd_status st = choose_head(c, &head); st != SCD_OK) return st;
   c->head_snap = getenv("SCD_HEAD_SNAP") && atoi(getenv("SCD_HEAD_SNAP")) == 1;
+  if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
   // launch order: longest coordinates first
   c->n_bins = 0;
   c->tau_star = 1e18;
@@ -334,6 +412,26 @@ scd_status build_schedule(scd_ctx *c) {
     if (v >= 1 && v <= kMaxSlices) c->n_slices = v;
   }
   if (scd_status st = setup_hot(c); st != SCD_OK) return st;
+  // tail read copy: a tail read may miss every update of the current slice, so it is kept only
+  // while a slice of the head bin stays within cap_fraction of the tail coupling's staleness bound
+  if (c->tail_snap) {
+    int bi = -1;
+    for (int i = 0; i < c->n_bins; ++i)
+      if (c->bins[i].head > 0 && c->bins[i].lanes == kLanesCta) bi = i;
+    bool keep = bi >= 0 && !c->head_snap;
+    if (keep) {
+      const Bin &B = c->bins[bi];
+      if (scd_status st = estimate_tail_tau(c, B.list, B.count, c->tail_lo, &c->tail_tau); st != SCD_OK) return st;
+      const double slice_rows = (double)B.count / (double)c->n_slices;
+      const bool forced = getenv("SCD_TAIL_SNAP") != nullptr;
+      keep = forced || (c->opt.max_inflight == 0 && slice_rows <= cap_fraction() * c->tail_tau);
+    }
+    if (!keep) {
+      cudaFree(c->svr);
+      c->svr = nullptr;
+      c->tail_snap = 0;
+    }
+  }
   // two ticket counters per (slice, bin): the second feeds die 1 of the die-split kernel
   SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices));
   return SCD_OK;

@@ -73,6 +73,18 @@ def test_head_kernel_schedule_and_convergence(c3p, monkeypatch):
     # rows in flight + pending head updates of `flush` rows per CTA: bounded by the staleness bound
     assert b["grid"] * (1 + b["flush"]) <= b["tau"], b
     assert not info["die_split"]
+    # tail read copy: only while one slice of the bin stays within half the tail coupling's bound
+    if info["tail_snap"]:
+        assert b["count"] / info["n_slices"] <= 0.5 * info["tail_tau"], info
+
+
+def test_tail_read_copy_convergence(c3p, monkeypatch):
+    """Head kernel with the tail gathers served from the per-slice read copy of w̄ (forced on: on
+    this 20 000-row prefix a slice is 1/8 of the rows, far staler than on the full C3)."""
+    monkeypatch.delenv("SCD_HEAD", raising=False)
+    monkeypatch.setenv("SCD_TAIL_SNAP", "1")
+    info = _converge(*c3p)
+    assert info["tail_snap"] == 1 and info["tail_tau"] > 0, info
 
 
 def test_head_kernel_off_matches_too(c3p, monkeypatch):
