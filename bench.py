@@ -289,6 +289,17 @@ def main():
                                  sink.data_ptr()) for _ in range(2))
         pattern = {"ms": pms, "entries_per_s": nnz / (pms / 1e3), "epoch_over_pattern": ms_step / pms,
                    "what": "gather + red.add of sv[idx] for every stored entry, storage order, no dependencies"}
+        if hasattr(pl, "pattern_run2"):
+            # the same with the gathers served from a second vector (the head kernel's tail read copy)
+            pl.pattern_run2.restype = C.c_float
+            pl.pattern_run2.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]
+            scratch2 = torch.zeros(cfg.n_cols + 1024, device="cuda")
+            pms2 = min(pl.pattern_run2(7, d["idx"].data_ptr(), d["val"].data_ptr(), nnz, scratch.data_ptr(),
+                                       scratch2.data_ptr(), sink.data_ptr()) for _ in range(2))
+            pattern["read_copy"] = {"ms": pms2, "entries_per_s": nnz / (pms2 / 1e3), "epoch_over_pattern": ms_step / pms2,
+                                    "what": "gather of a second vector + red.add of sv[idx] for every stored entry"}
+            del scratch2
         del scratch
 
     # time to duality gap 1e-4 from a fresh start (epoch + aggregation time only, gap off the clock)

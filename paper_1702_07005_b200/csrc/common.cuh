@@ -157,6 +157,7 @@ struct scd_ctx {
   bool hot_view = false;              // hot-set kernel also keeps a per-CTA view of the hot values
   double hot_cover = 0.0;             // share of the bin's entries that are hot
   bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)
+  bool head_pf = true;                // head kernel prefetches the next coordinate (SCD_HEAD_PF=0: off)
   int tail_snap = 0;                  // head kernel reads the tail [tail_lo, tail_hi) of the shared vector from a
                                       // read copy refreshed before every slice: 1 = L2 loads, 2 = L1-cached loads
   float *svr = nullptr;               // device [n_shared]: the read copy (only [tail_lo, tail_hi) is maintained)

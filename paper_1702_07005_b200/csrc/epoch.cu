@@ -346,7 +346,12 @@ __device__ __forceinline__ float ld_tail(const EpochArgs &a, int32_t j) {
   return ld_sv(a.sv + j);
 }
 
-template <int FORM, int T, int E, bool SNAP, int TS = 0>
+// PF: thread 0 prefetches the next coordinate (ticket, permutation, offsets, model, norm, label)
+// while the CTA works on the current one and publishes it through shared memory, so the
+// ticket -> Feistel -> ptr -> x chain (three dependent round trips) leaves the per-row critical
+// path.  The prefetched coordinate reads nothing of the shared vector before its turn, so this adds
+// no staleness; x[c'] is current because this CTA is its only writer in the epoch (c10).
+template <int FORM, int T, int E, bool SNAP, int TS = 0, bool PF = false>
 __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
   constexpr int NW = T / 32;
   extern __shared__ float4 s_dyn[];
@@ -355,20 +360,56 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
   __shared__ float s_red[NW];
   __shared__ float s_delta;
   __shared__ unsigned int s_ticket;
+  __shared__ int64_t s_cur[3];  // PF: coordinate (-1 = slice done), ptr[c], ptr[c + 1]
+  __shared__ float s_cx[3];     // PF: x[c], norm[c], y[c]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int i = tid; i < H; i += T) s_acc[i] = b.dry ? -0.f : 0.f;
   if (SNAP) {
     __syncthreads();
     head_flush<T, true>(a.sv, s_acc, s_w, H, 0);  // initial view (nothing pending yet)
   }
+  int64_t n_c = -1, n_beg = 0, n_end = 0;  // PF (thread 0): the next coordinate
+  float n_x = 0.f, n_nrm = 0.f, n_y = 0.f;
+  unsigned n_tk = 0;
+  auto fetch = [&](unsigned tk) {
+    const int64_t t = b.lo + (int64_t)tk;
+    n_c = -1;
+    if (t >= b.hi) return;
+    n_c = bin_coord(b, t);
+    n_beg = __ldg(a.ptr + n_c);
+    n_end = __ldg(a.ptr + n_c + 1);
+    n_x = a.x[n_c];
+    n_nrm = __ldg(a.norm + n_c);
+    n_y = FORM == SCD_DUAL ? __ldg(a.y + n_c) : 0.f;
+  };
+  if (PF && tid == 0) fetch(atomicAdd(b.counter, 1u));
   int since = 0;
   for (;;) {
-    if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
-    __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
-    const int64_t t = b.lo + (int64_t)s_ticket;
-    if (t >= b.hi) break;
-    const int64_t c = bin_coord(b, t);
-    const int64_t beg = __ldg(a.ptr + c), end = __ldg(a.ptr + c + 1);
+    int64_t c, beg, end;
+    if (PF) {
+      if (tid == 0) {
+        s_cur[0] = n_c;
+        s_cur[1] = n_beg;
+        s_cur[2] = n_end;
+        s_cx[0] = n_x;
+        s_cx[1] = n_nrm;
+        s_cx[2] = n_y;
+        if (n_c >= 0) n_tk = atomicAdd(b.counter, 1u);  // consumed after this row's gathers
+      }
+      __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
+      c = s_cur[0];
+      if (c < 0) break;
+      beg = s_cur[1];
+      end = s_cur[2];
+    } else {
+      if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
+      __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
+      const int64_t t = b.lo + (int64_t)s_ticket;
+      if (t >= b.hi) break;
+      c = bin_coord(b, t);
+      beg = __ldg(a.ptr + c);
+      end = __ldg(a.ptr + c + 1);
+    }
     int32_t id[E];
     float v[E];
     float acc = 0.f;
@@ -412,6 +453,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
         }
       }
     }
+    if (PF && tid == 0 && c >= 0) fetch(n_tk);  // next coordinate's chain overlaps reduce + scatter
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -419,9 +461,10 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
       float s = lane < NW ? s_red[lane] : 0.f;
       s = warp_sum(s);
       if (lane == 0) {
-        const float xc = a.x[c];
-        const float d = coord_delta<FORM>(s, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f,
-                                          a.lam, a.lamN);
+        const float xc = PF ? s_cx[0] : a.x[c];
+        const float nc = PF ? s_cx[1] : __ldg(a.norm + c);
+        const float yc = PF ? s_cx[2] : (FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f);
+        const float d = coord_delta<FORM>(s, xc, nc, yc, a.lam, a.lamN);
         if (!b.dry) a.x[c] = xc + d;  // single writer per epoch (c10)
         s_delta = b.dry ? 0.f : d;
       }
@@ -1263,9 +1306,13 @@ void *bin_kernel(const scd_ctx *c, const Bin &b) {
   if (b.split && b.lanes == kLanesCta)
     return c->form == SCD_PRIMAL ? (void *)k_epoch_split<SCD_PRIMAL, kCtaT, kCtaE>
                                  : (void *)k_epoch_split<SCD_DUAL, kCtaT, kCtaE>;
-  if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && !c->head_snap && c->form == SCD_DUAL)
+  if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && !c->head_snap && c->form == SCD_DUAL) {
+    if (c->head_pf)
+      return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 2, true>
+                               : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true>;
     return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 2>
                              : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1>;
+  }
   if (b.head > 0 && b.lanes == kLanesCta)
     return c->head_snap ? (c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE, true>
                                                  : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true>)

@@ -380,6 +380,7 @@ scd_status build_schedule(scd_ctx *c) {
   if (scd_status st = choose_head(c, &head); st != SCD_OK) return st;
   c->head_snap = getenv("SCD_HEAD_SNAP") && atoi(getenv("SCD_HEAD_SNAP")) == 1;
   if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
+  c->head_pf = !(getenv("SCD_HEAD_PF") && atoi(getenv("SCD_HEAD_PF")) == 0);
   // launch order: longest coordinates first
   c->n_bins = 0;
   c->tau_star = 1e18;

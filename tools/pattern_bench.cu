@@ -6,9 +6,11 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// MODE bit 0: gather, bit 1: RED, bit 2: gather from svr (a second vector: the epoch kernels' tail
+// read copy) instead of sv
 template <int MODE>
 __global__ void __launch_bounds__(256) k_pattern(const int32_t *__restrict__ idx, const float *__restrict__ val,
-                                                 int64_t nnz, float *sv, float *sink) {
+                                                 int64_t nnz, float *sv, float *sink, const float *svr = nullptr) {
   float acc = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += 4 * stride) {
@@ -23,7 +25,7 @@ __global__ void __launch_bounds__(256) k_pattern(const int32_t *__restrict__ idx
     if (MODE & 1) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (id[u] >= 0) acc += __ldcg(sv + id[u]) * v[u];
+        if (id[u] >= 0) acc += __ldcg((MODE & 4 ? svr : sv) + id[u]) * v[u];
     }
     if (MODE & 2) {
 #pragma unroll
@@ -34,7 +36,8 @@ __global__ void __launch_bounds__(256) k_pattern(const int32_t *__restrict__ idx
   if (acc == 1.2345f) sink[0] = acc;
 }
 
-extern "C" float pattern_run(int mode, const int32_t *idx, const float *val, int64_t nnz, float *sv, float *sink) {
+extern "C" float pattern_run2(int mode, const int32_t *idx, const float *val, int64_t nnz, float *sv, const float *svr,
+                              float *sink) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t a, b;
@@ -46,6 +49,7 @@ extern "C" float pattern_run(int mode, const int32_t *idx, const float *val, int
   if (mode == 1) k_pattern<1><<<grid, 256>>>(idx, val, nnz, sv, sink);
   if (mode == 2) k_pattern<2><<<grid, 256>>>(idx, val, nnz, sv, sink);
   if (mode == 3) k_pattern<3><<<grid, 256>>>(idx, val, nnz, sv, sink);
+  if (mode == 7) k_pattern<7><<<grid, 256>>>(idx, val, nnz, sv, sink, svr);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0.f;
@@ -53,4 +57,8 @@ extern "C" float pattern_run(int mode, const int32_t *idx, const float *val, int
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   return ms;
+}
+
+extern "C" float pattern_run(int mode, const int32_t *idx, const float *val, int64_t nnz, float *sv, float *sink) {
+  return pattern_run2(mode, idx, val, nnz, sv, nullptr, sink);
 }
