@@ -349,12 +349,22 @@ scd_status build_schedule(scd_ctx *c) {
   // bin thresholds (entries per coordinate): (0,64] -> 8-lane groups, (64,1024] -> warps,
   // (1024,16384] -> one CTA, > 16384 -> one 8-CTA cluster per coordinate
   constexpr int NB = 4;
-  const int64_t lim[NB] = {64, 1024, 16384, INT64_MAX};
   int lanes[NB] = {8, 32, kLanesCta, kLanesCluster};
   if (const char *e = getenv("SCD_SHORT_LANES")) {  // tuning: lanes per short coordinate (8, 16 or 32)
     const int l = atoi(e);
     if (l == 8 || l == 16 || l == 32) lanes[0] = l;
   }
+  int head = 0;
+  if (scd_status st = choose_head(c, &head); st != SCD_OK) return st;
+  // with the head-combining CTA kernel the medium rows (64, 1024] join the CTA bin (dual only): a
+  // separate warp-bin launch per slice is a latency-bound single wave (C3: 2.5% of the step for 0.7%
+  // of the entries); SCD_HEAD_MIN sets the shortest row of the CTA bin (default 65)
+  int64_t lim1 = 1024;
+  if (head > 0 && c->form == SCD_DUAL) {
+    lim1 = 64;
+    if (const char *e = getenv("SCD_HEAD_MIN")) lim1 = std::max<int64_t>(64, std::min<int64_t>(1024, atoll(e) - 1));
+  }
+  const int64_t lim[NB] = {64, lim1, 16384, INT64_MAX};
   std::vector<int32_t> lists[NB], empty;
   int64_t nnzb[NB] = {0, 0, 0, 0};
   for (int64_t i = 0; i < n; ++i) {
@@ -376,8 +386,6 @@ scd_status build_schedule(scd_ctx *c) {
     SCD_CK(c, cudaMalloc((void **)&c->empty_list, sizeof(int32_t) * empty.size()));
     SCD_CK(c, cudaMemcpy(c->empty_list, empty.data(), sizeof(int32_t) * empty.size(), cudaMemcpyHostToDevice));
   }
-  int head = 0;
-  if (scd_status st = choose_head(c, &head); st != SCD_OK) return st;
   c->head_snap = getenv("SCD_HEAD_SNAP") && atoi(getenv("SCD_HEAD_SNAP")) == 1;
   if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
   c->head_pf = !(getenv("SCD_HEAD_PF") && atoi(getenv("SCD_HEAD_PF")) == 0);
@@ -407,7 +415,7 @@ scd_status build_schedule(scd_ctx *c) {
     ++c->n_bins;
   }
   // interleave the bins in slices when more than one bin carries work (reading c24)
-  c->n_slices = c->n_bins > 1 ? 8 : 1;
+  c->n_slices = (c->n_bins > 1 || (head > 0 && c->tail_snap)) ? 8 : 1;
   if (const char *e = getenv("SCD_SLICES")) {
     int v = atoi(e);
     if (v >= 1 && v <= kMaxSlices) c->n_slices = v;
