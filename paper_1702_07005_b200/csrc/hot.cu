@@ -9,6 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -97,7 +98,15 @@ scd_status setup_hot(scd_ctx *c) {
       c->hot_ids = nullptr;
     } else {
       int32_t *slot_of = reinterpret_cast<int32_t *>(cnt);  // reuse: n int32
-      cudaMemcpyAsync(c->hot_ids, ids_sorted, sizeof(int32_t) * kk, cudaMemcpyDeviceToDevice, s);
+      // slots in shared-vector order (SCD_HOT_ORDER=freq: most frequent first): the top values of a
+      // frequency-ranked field are consecutive ids, so a warp's flush REDs over 32 consecutive slots
+      // coalesce into a few sector operations instead of 32 on the hottest lines
+      std::vector<int32_t> hid((size_t)kk);
+      cudaMemcpyAsync(hid.data(), ids_sorted, sizeof(int32_t) * kk, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      const char *ord = getenv("SCD_HOT_ORDER");
+      if (!(ord && std::string(ord) == "freq")) std::sort(hid.begin(), hid.end());
+      cudaMemcpyAsync(c->hot_ids, hid.data(), sizeof(int32_t) * kk, cudaMemcpyHostToDevice, s);
       cudaMemsetAsync(slot_of, 0xff, sizeof(int32_t) * n, s);
       k_hot_slots<<<grid_for(kk, 256), 256, 0, s>>>(c->hot_ids, (int)kk, slot_of);
       k_hot_encode<<<grid_for(c->nnz, 256, 148 * 16), 256, 0, s>>>(c->idx, c->nnz, slot_of, c->hot_idx);

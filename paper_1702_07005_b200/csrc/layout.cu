@@ -265,9 +265,7 @@ static scd_status setup_tail_snap(scd_ctx *c, int head) {
   if (h < head) return SCD_OK;
   c->tail_lo = head;
   c->tail_hi = (int64_t)h + 1;
-  SCD_CK(c, cudaMalloc((void **)&c->svr, sizeof(float) * (size_t)c->n_shared));
-  SCD_CK(c, cudaMemsetAsync(c->svr, 0, sizeof(float) * (size_t)c->n_shared, c->stream));
-  c->tail_snap = mode;
+  c->tail_snap = mode;  // the copy is allocated once the schedule keeps it (build_schedule)
   return SCD_OK;
 }
 
@@ -414,15 +412,17 @@ scd_status build_schedule(scd_ctx *c) {
     bin_launch_shape(c, B);
     ++c->n_bins;
   }
-  // interleave the bins in slices when more than one bin carries work (reading c24)
-  c->n_slices = (c->n_bins > 1 || (head > 0 && c->tail_snap)) ? 8 : 1;
-  if (const char *e = getenv("SCD_SLICES")) {
-    int v = atoi(e);
-    if (v >= 1 && v <= kMaxSlices) c->n_slices = v;
-  }
   if (scd_status st = setup_hot(c); st != SCD_OK) return st;
-  // tail read copy: a tail read may miss every update of the current slice, so it is kept only
-  // while a slice of the head bin stays within cap_fraction of the tail coupling's staleness bound
+  // interleave the bins in slices when more than one bin carries work (reading c24); SCD_SLICES overrides
+  int S_env = 0;
+  if (const char *e = getenv("SCD_SLICES")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= kMaxSlices) S_env = v;
+  }
+  int S = c->n_bins > 1 ? 8 : 1;
+  // tail read copy: refreshed before every slice, so a tail read may miss every update of the current
+  // slice; it is kept only while a slice of the head bin (8 slices, or SCD_SLICES) stays within
+  // cap_fraction of the tail coupling's staleness bound
   if (c->tail_snap) {
     int bi = -1;
     for (int i = 0; i < c->n_bins; ++i)
@@ -431,16 +431,19 @@ scd_status build_schedule(scd_ctx *c) {
     if (keep) {
       const Bin &B = c->bins[bi];
       if (scd_status st = estimate_tail_tau(c, B.list, B.count, c->tail_lo, &c->tail_tau); st != SCD_OK) return st;
-      const double slice_rows = (double)B.count / (double)c->n_slices;
+      const double slice_rows = (double)B.count / (double)(S_env ? S_env : 8);
       const bool forced = getenv("SCD_TAIL_SNAP") != nullptr;
       keep = forced || (c->opt.max_inflight == 0 && slice_rows <= cap_fraction() * c->tail_tau);
     }
-    if (!keep) {
-      cudaFree(c->svr);
-      c->svr = nullptr;
+    if (keep) {
+      SCD_CK(c, cudaMalloc((void **)&c->svr, sizeof(float) * (size_t)c->n_shared));
+      SCD_CK(c, cudaMemsetAsync(c->svr, 0, sizeof(float) * (size_t)c->n_shared, c->stream));
+      S = 8;
+    } else {
       c->tail_snap = 0;
     }
   }
+  c->n_slices = S_env ? S_env : S;
   // two ticket counters per (slice, bin): the second feeds die 1 of the die-split kernel
   SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices));
   return SCD_OK;
