@@ -1306,6 +1306,9 @@ void *bin_kernel(const scd_ctx *c, const Bin &b) {
   if (b.split && b.lanes == kLanesCta)
     return c->form == SCD_PRIMAL ? (void *)k_epoch_split<SCD_PRIMAL, kCtaT, kCtaE>
                                  : (void *)k_epoch_split<SCD_DUAL, kCtaT, kCtaE>;
+  if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && c->head_snap && c->form == SCD_DUAL)
+    return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true, 2>
+                             : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true, 1>;
   if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && !c->head_snap && c->form == SCD_DUAL) {
     if (c->head_pf)
       return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 2, true>
@@ -1570,7 +1573,7 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       int64_t grid = b.grid / unit;
       if (grid > need) grid = need;
       if (grid < 1) grid = 1;
-      if (c->tail_snap && b.head > 0 && b.lanes == kLanesCta && !c->head_snap) {
+      if (c->tail_snap && b.head > 0 && b.lanes == kLanesCta) {
         k_tail_refresh<<<c->nsm * 4, 256, 0, s>>>(c->sv, c->svr, c->tail_lo, c->tail_hi);
         SCD_CKL(c, "k_tail_refresh launch");
         ++c->launches;

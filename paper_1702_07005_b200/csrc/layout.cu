@@ -427,7 +427,7 @@ scd_status build_schedule(scd_ctx *c) {
     int bi = -1;
     for (int i = 0; i < c->n_bins; ++i)
       if (c->bins[i].head > 0 && c->bins[i].lanes == kLanesCta) bi = i;
-    bool keep = bi >= 0 && !c->head_snap;
+    bool keep = bi >= 0;
     if (keep) {
       const Bin &B = c->bins[bi];
       if (scd_status st = estimate_tail_tau(c, B.list, B.count, c->tail_lo, &c->tail_tau); st != SCD_OK) return st;
