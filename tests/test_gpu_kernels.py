@@ -195,3 +195,43 @@ def test_hot_set_kernel_ragged_short_rows(monkeypatch):
     print("seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(finals["4096"] - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert abs(finals["0"] - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
+
+
+def test_tail_read_copy_ragged_two_bins(monkeypatch):
+    """Head kernel + tail read copy on ragged rows (16..5000 entries: an 8-lane bin beside the CTA
+    bin, medium rows merged into the CTA bin), a small head (H = 1024) and a tail range whose length is
+    not a multiple of 4 (scalar tail of k_tail_refresh).  Checked against the oracle's optimum and
+    sequential band, and w̄ returned by the library against Aᵀα recomputed in fp64 (the copy must never
+    leak into the shared vector itself)."""
+    monkeypatch.setenv("SCD_HEAD", "1024")
+    monkeypatch.setenv("SCD_TAIL_SNAP", "1")
+    cfg = synth.ZipfRowsCfg("ragged_head", 20_000, 50_003, 40_001, 1.0, 600.0, 1.0, 16, 5000, seed=11)
+    d = synth.gen_host(cfg)
+    pr = solver.Problem.from_csr(d, lam=1e-3 * 350_000 / 20_000)
+    _, _, hist = solver.solve(pr, "dual", E, seed=7)
+    s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=7)
+    info = s.info()
+    print("schedule", info)
+    assert info["tail_snap"] == 1, info
+    lanes = sorted(b["lanes"] for b in info["bins"])
+    assert lanes == [8, 256], lanes  # (64, 1024] rows joined the CTA bin
+    cta = [b for b in info["bins"] if b["lanes"] == 256][0]
+    assert cta["head"] == 1024, cta
+    assert int(d["idx"].max()) + 1 - 1024 > 0 and (int(d["idx"].max()) + 1 - 1024) % 4 != 0
+    gaps = []
+    for t in range(1, E + 1):
+        s.epoch(t)
+        gaps.append(s.duality_gap())
+    x = s.get_model().astype(np.float64)
+    wbar = s.get_shared().astype(np.float64)
+    s.close()
+    A = pr.A()
+    v = A.T @ x
+    print("gpu gaps", ["%.2e" % g for g in gaps])
+    print("seq gaps", ["%.2e" % h["gap"] for h in hist])
+    assert np.abs(wbar - v).max() <= 1e-4 * np.abs(v).max()
+    Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+    assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
+    assert gaps[-1] <= 1e-5
+    for t in (0, 1, 3):
+        assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
