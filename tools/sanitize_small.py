@@ -1,6 +1,7 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer (memcheck / racecheck):
 deterministic and asynchronous epochs (CTA, sub-warp, combining, cluster bins), the head-combining
-CTA kernel (plain and with the shared-memory view), the die-split kernel, the wild scatter, the
+CTA kernel (plain, with the shared-memory view, with the tail read copy and next-coordinate
+prefetch), the die-split kernel, the wild scatter, the
 hot-set kernel (and its view), the fused peer-memory aggregation, device renumbering, empty
 rows/cols, implicit values, gap/objective, aggregation (group and 1-rank NCCL), transpose,
 permutation."""
@@ -70,12 +71,15 @@ for form in ("dual", "primal"):
 # covering every SM: head-combining kernel, its shared-memory view, and the die-split kernel
 c3 = synth.gen_host(synth.CONFIGS["C3"].with_rows(1500))
 c3["lam"] = 350.0 / 1500
-for env in ({}, {"SCD_HEAD_SNAP": "1", "SCD_HEAD_FLUSH": "2"}, {"SCD_DIE_SPLIT": "1"}):
+for env in ({}, {"SCD_HEAD_SNAP": "1", "SCD_HEAD_FLUSH": "2"}, {"SCD_DIE_SPLIT": "1"},
+            {"SCD_HEAD_FLUSH": "2", "SCD_TAIL_SNAP": "1"}, {"SCD_HEAD_FLUSH": "2", "SCD_TAIL_SNAP": "1", "SCD_HEAD_PF": "0"},
+            {"SCD_HEAD_FLUSH": "2", "SCD_TAIL_SNAP": "2", "SCD_HEAD_SNAP": "1"}):
     os.environ.update(env)
     s = scd.Solver(c3["ptr"], c3["idx"], c3["val"], 1500, c3["n_cols"], c3["y"], c3["lam"], "dual", seed=3)
     inf = s.info()
     s.close()
-    print("c3 prefix", env, inf["bins"][0], "die_split", inf["die_split"], run(c3, "dual"), flush=True)
+    print("c3 prefix", env, inf["bins"][0], "die_split", inf["die_split"], "tail_snap", inf["tail_snap"],
+          run(c3, "dual"), flush=True)
     for k in env:
         del os.environ[k]
 # criteo-shaped rows with λN = 2e5 (as in the 8-GPU shards): the hot-set kernel (and its view variant)
