@@ -200,6 +200,8 @@ typedef struct {
                              refreshed before every slice; 0 = off */
   double tail_tau;        /* staleness bound of the coupling through the tail entries (coordinates); the
                              tail copy is used only while a slice's coordinates are <= tail_tau / 2 */
+  int32_t bin_snap[4];    /* per bin: 1 = each slice launch gathers from a copy of the shared vector taken just
+                             before it (the slice's coordinates are within the bin's in-flight cap) */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

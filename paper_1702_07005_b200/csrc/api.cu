@@ -492,6 +492,7 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
     info->bin_flush[i] = c->bins[i].flush;
     info->bin_split[i] = c->bins[i].split;
     info->bin_hot[i] = c->bins[i].hot;
+    info->bin_snap[i] = c->bins[i].snap;
     if (c->bins[i].cap > info->inflight_cap) info->inflight_cap = c->bins[i].cap;
   }
   return SCD_OK;

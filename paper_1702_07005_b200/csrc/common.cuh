@@ -93,6 +93,8 @@ struct Bin {
   int split = 0;             // CTA bins: 1 = die-split kernel (k_epoch_split, die.cu)
   int cl = kClusterCtas;     // cluster bin: CTAs per cluster (one coordinate per cluster)
   int hot = 0;               // 8-lane bin: > 0 = hot-set kernel with this many hot slots (hot.cu)
+  int snap = 0;              // 1 = every slice launch gathers from a copy of the shared vector taken just
+                             // before it (the whole slice within the bin's staleness cap)
   int64_t count = 0, nnz = 0;
   int32_t *list = nullptr;   // device, coordinate ids ascending
   int grid = 0, block = 0;

@@ -37,6 +37,7 @@ struct EpochArgs {
   float *x;
   float *sv;
   const float *svr;  // head kernel with a tail read copy: gathers of ids >= H read svr (else == sv)
+  const float *svg;  // gather source of the plain kernels: sv, or svr for a snapshot bin (Bin::snap)
   double lam, lamN;
 };
 
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (id[u] >= 0) acc = fmaf(ld_sv(a.sv + id[u]), v[u], acc);
+        if (id[u] >= 0) acc = fmaf(ld_sv(a.svg + id[u]), v[u], acc);
     }
     if (tid == 0) {  // schedule the next coordinate while the block reduces / scatters
       const int64_t t = b.lo + (int64_t)nticket;
@@ -266,9 +267,9 @@ __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.svg + id[e]), v[e], acc);
     // remaining chunks of a long coordinate (re-read for the scatter; L2-resident by then)
-    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T);
+    acc += dot_strided<8>(a.svg, a.idx, a.val, beg + (int64_t)T * E + tid, end, T);
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -660,8 +661,8 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G);
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.svg + id[e]), v[e], acc);
+    acc += dot_strided<8>(a.svg, a.idx, a.val, beg + (int64_t)G * E + gl, end, G);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     float d = 0.f;
@@ -753,8 +754,8 @@ __global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b
     float acc = 0.f;
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G);
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.svg + id[e]), v[e], acc);
+    acc += dot_strided<8>(a.svg, a.idx, a.val, beg + (int64_t)G * E + gl, end, G);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
     // (c) delta of batch i (group leader is the single writer of x[c], c10)
@@ -901,7 +902,7 @@ __global__ void __launch_bounds__(T) k_epoch_group_comb(EpochArgs a, BinArgs b) 
     const int n = s_n;
     for (int i = tid; i < n; i += T) {  // one gather per distinct entry
       const int h = s_list[i];
-      s_g[h] = ld_sv(a.sv + s_key[h]);
+      s_g[h] = ld_sv(a.svg + s_key[h]);
       s_r[h] = 0.f;
     }
     __syncthreads();
@@ -1199,8 +1200,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    acc += dot_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)T * E + tid, end, T);
+      if (id[e] >= 0) acc = fmaf(ld_sv(a.svg + id[e]), v[e], acc);
+    acc += dot_strided<8>(a.svg, a.idx, a.val, beg + (int64_t)T * E + tid, end, T);
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -1334,6 +1335,7 @@ EpochArgs make_args(scd_ctx *c) {
   a.x = c->x;
   a.sv = c->sv;
   a.svr = c->tail_snap ? c->svr : c->sv;
+  a.svg = c->sv;
   a.lam = c->lam;
   a.lamN = c->lamN;
   return a;
@@ -1578,13 +1580,20 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
         SCD_CKL(c, "k_tail_refresh launch");
         ++c->launches;
       }
+      EpochArgs ab = a;
+      if (b.snap) {  // snapshot bin: the whole slice launch gathers from a copy taken just before it
+        k_tail_refresh<<<c->nsm * 4, 256, 0, s>>>(c->sv, c->svr, 0, c->n_shared);
+        SCD_CKL(c, "k_tail_refresh launch");
+        ++c->launches;
+        ab.svg = c->svr;
+      }
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (c->opt.profile) {
         e0 = get_event(c);
         e1 = get_event(c);
         cudaEventRecord(e0, s);
       }
-      scd_status st = launch_bin(c, b, a, ba, grid * unit, s);
+      scd_status st = launch_bin(c, b, ab, ba, grid * unit, s);
       if (st != SCD_OK) return st;
       ++c->launches;
       if (c->opt.profile) {

@@ -444,6 +444,32 @@ scd_status build_schedule(scd_ctx *c) {
     }
   }
   c->n_slices = S_env ? S_env : S;
+  // Snapshot bins: when one slice launch of a bin holds no more coordinates than the bin's in-flight
+  // cap (cap_fraction * τ_b), the whole launch may gather from a copy of the shared vector taken
+  // just before it — the same block-Jacobi bound as the in-flight cap, with the whole slice counted
+  // as in flight — so the lines gathered and the lines reduced are disjoint.  Plain
+  // kernels only; the copy refresh must stay small next to the slice's own traffic.  SCD_BIN_SNAP=0: off.
+  const bool snap_ok = !(getenv("SCD_BIN_SNAP") && atoi(getenv("SCD_BIN_SNAP")) == 0) && !c->opt.deterministic &&
+                       !c->opt.wild && c->opt.max_inflight == 0;
+  bool any_snap = false;
+  for (int i = 0; i < c->n_bins && snap_ok; ++i) {
+    Bin &B = c->bins[i];
+    B.snap = 0;
+    if (B.head > 0 || B.hot > 0 || B.split) continue;
+    const double slice = (double)B.count / (double)c->n_slices;
+    const double refresh_bytes = 8.0 * (double)c->n_shared, slice_bytes = 16.0 * (double)B.nnz / c->n_slices;
+    // like the combined-update windows (combine_window, reading c25) a slice may also be at most 1/8
+    // of the bin: the bound keeps the step contractive, the 1/8 keeps the per-epoch rate sequential-like
+    // (a whole-epoch snapshot is a Jacobi epoch and converges visibly slower per epoch)
+    if (slice <= cap_fraction() * B.tau && slice <= (double)B.count / 8.0 + 1.0 && refresh_bytes <= 0.05 * slice_bytes) {
+      B.snap = 1;
+      any_snap = true;
+    }
+  }
+  if (any_snap && !c->svr) {
+    SCD_CK(c, cudaMalloc((void **)&c->svr, sizeof(float) * (size_t)c->n_shared));
+    SCD_CK(c, cudaMemsetAsync(c->svr, 0, sizeof(float) * (size_t)c->n_shared, c->stream));
+  }
   // two ticket counters per (slice, bin): the second feeds die 1 of the die-split kernel
   SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices));
   return SCD_OK;

@@ -201,12 +201,25 @@ def test_async_converges_to_oracle_optimum(c2full, form):
     xs, _, hist = solver.solve(pr, form, E, seed=4)
     args = (d["ptr"], d["idx"], d["val"]) if form == "dual" else (pr.cptr, pr.cidx, pr.cval)
     s = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=4)
-    print("schedule", s.info())
+    info = s.info()
+    print("schedule", info)
+    # snapshot bins (whole slice gathers from a copy): only within the bin's cap and 1/8
+    for b in info["bins"]:
+        if b["snap"]:
+            assert b["count"] / info["n_slices"] <= min(b["cap"] + 1, b["count"] / 8 + 1), b
+    if form == "primal":
+        assert any(b["snap"] for b in info["bins"]), info  # the C2 primal warp bin qualifies
     gaps = []
     for t in range(1, E + 1):
         s.epoch(t)
         gaps.append(s.duality_gap())
     x = s.get_model().astype(np.float64)
+    # the library's shared vector stays the one of the model (the copies never leak into it)
+    sh = s.get_shared().astype(np.float64)
+    ref = A.T @ x if form == "dual" else A @ x
+    # fp32 atomics accumulate ~2e4 updates per entry over 20 epochs: drift ~1e-4 of the largest entry;
+    # a leaked copy or a lost update would be O(1)
+    assert np.abs(sh - ref).max() <= 1e-3 * max(np.abs(ref).max(), 1e-30)
     if form == "dual":
         Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
     else:
