@@ -164,6 +164,8 @@ struct scd_ctx {
                                       // read copy refreshed before every slice: 1 = L2 loads, 2 = L1-cached loads
   float *svr = nullptr;               // device [n_shared]: the read copy (only [tail_lo, tail_hi) is maintained)
   int64_t tail_lo = 0, tail_hi = 0;
+  int64_t sv_active = 0;              // dual: w̄ is zero beyond [0, sv_active) on every rank (aggregation extent)
+  bool sv_active_global = false;      // sv_active already reduced (max) over the ranks
   double tail_tau = 0.0;              // staleness bound of the head bin's coupling through the tail entries
   bool die_split = false;
   uint8_t *sm_die = nullptr;          // device [kMaxSm]: die of each SM id

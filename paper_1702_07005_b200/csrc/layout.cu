@@ -249,11 +249,11 @@ static scd_status choose_head(scd_ctx *c, int *head) {
 // Tail read copy of the head kernel: the gathers of tail entries (ids >= H) are served
 // from svr, a copy of sv[H, max id] refreshed before every slice, so the lines that are gathered and
 // the lines that take REDs are disjoint.  SCD_TAIL_SNAP = 1 (L2 loads) | 2 (L1-cached loads) | 0.
-static scd_status setup_tail_snap(scd_ctx *c, int head) {
-  c->tail_snap = 0;
-  const char *e = getenv("SCD_TAIL_SNAP");
-  const int mode = e ? atoi(e) : 1;
-  if (head <= 0 || (mode != 1 && mode != 2) || c->form != SCD_DUAL) return SCD_OK;
+// Largest inner index + 1 of the local matrix (0 if empty): the dual's w̄ is zero beyond it, so the
+// aggregation only exchanges [0, sv_active) (the max over all ranks, taken at the first round).
+static scd_status active_extent(scd_ctx *c, int64_t *out) {
+  *out = 0;
+  if (c->nnz == 0) return SCD_OK;
   int *d = nullptr, h = -1;
   SCD_CK(c, cudaMallocAsync((void **)&d, sizeof(int), c->stream));
   SCD_CK(c, cudaMemsetAsync(d, 0xff, sizeof(int), c->stream));
@@ -262,6 +262,16 @@ static scd_status setup_tail_snap(scd_ctx *c, int head) {
   SCD_CK(c, cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   SCD_CK(c, cudaStreamSynchronize(c->stream));
   cudaFreeAsync(d, c->stream);
+  *out = (int64_t)h + 1;
+  return SCD_OK;
+}
+
+static scd_status setup_tail_snap(scd_ctx *c, int head) {
+  c->tail_snap = 0;
+  const char *e = getenv("SCD_TAIL_SNAP");
+  const int mode = e ? atoi(e) : 1;
+  if (head <= 0 || (mode != 1 && mode != 2) || c->form != SCD_DUAL) return SCD_OK;
+  const int64_t h = c->sv_active - 1;
   if (h < head) return SCD_OK;
   c->tail_lo = head;
   c->tail_hi = (int64_t)h + 1;
@@ -385,6 +395,11 @@ scd_status build_schedule(scd_ctx *c) {
     SCD_CK(c, cudaMemcpy(c->empty_list, empty.data(), sizeof(int32_t) * empty.size(), cudaMemcpyHostToDevice));
   }
   c->head_snap = getenv("SCD_HEAD_SNAP") && atoi(getenv("SCD_HEAD_SNAP")) == 1;
+  c->sv_active = c->n_shared;
+  if (c->form == SCD_DUAL) {
+    if (scd_status st = active_extent(c, &c->sv_active); st != SCD_OK) return st;
+    c->sv_active = std::max<int64_t>(1, std::min(c->sv_active, c->n_shared));
+  }
   if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
   c->head_pf = !(getenv("SCD_HEAD_PF") && atoi(getenv("SCD_HEAD_PF")) == 0);
   // launch order: longest coordinates first

@@ -404,3 +404,26 @@ def test_fused_peer_aggregation_single_rank(c2s, form, monkeypatch):
     np.testing.assert_array_equal(a.get_shared(), b.get_shared())
     a.close()
     scd.nccl_comm_destroy(comm)
+
+
+def test_aggregate_active_extent_dual():
+    """The dual's aggregation exchanges only [0, largest inner index] of w̄, which is zero beyond it
+    on every rank.  With the last 37 columns empty the rounds must still equal the
+    Alg. 4 simulator (K = 1, optimal γ, oracle) and leave w̄ = 0 beyond the extent."""
+    d = synth.random_sparse(300, 200, 0.05, seed=21, empty_cols=37)
+    pr = solver.Problem.from_csr(d, lam=d["lam"])
+    x_o, s_o, hist = solver.run_distributed(pr, "dual", 1, "optimal", 3, seed=5, seed_part=9)
+    s = scd.Solver(d["ptr"], d["idx"], d["val"], 300, 200, d["y"], d["lam"], "dual", seed=5, deterministic=True)
+    gam = []
+    for t in (1, 2, 3):
+        s.epoch(t)
+        gam.append(s.aggregate("optimal"))
+    x = s.get_model().astype(np.float64)
+    wbar = s.get_shared().astype(np.float64)
+    s.close()
+    assert int(d["idx"].max()) < 200 - 37
+    for g, h in zip(gam, hist):
+        assert g == pytest.approx(h["gamma"], rel=1e-4, abs=1e-6), (gam, [h["gamma"] for h in hist])
+    assert np.abs(x - x_o).max() <= 1e-4 * np.abs(x_o).max()
+    assert np.abs(wbar - s_o).max() <= 1e-4 * np.abs(s_o).max()
+    assert not wbar[200 - 37:].any()
