@@ -202,6 +202,8 @@ typedef struct {
                              tail copy is used only while a slice's coordinates are <= tail_tau / 2 */
   int32_t bin_snap[4];    /* per bin: 1 = each slice launch gathers from a copy of the shared vector taken just
                              before it (the slice's coordinates are within the bin's in-flight cap) */
+  int64_t tail_roll;      /* > 0: the tail copy is refreshed inside the epoch, one 1024-float chunk every tail_roll
+                             rows (no slice boundaries); 0 = refreshed between slices */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

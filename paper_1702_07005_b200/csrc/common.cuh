@@ -167,6 +167,8 @@ struct scd_ctx {
   int64_t sv_active = 0;              // dual: w̄ is zero beyond [0, sv_active) on every rank (aggregation extent)
   bool sv_active_global = false;      // sv_active already reduced (max) over the ranks
   double tail_tau = 0.0;              // staleness bound of the head bin's coupling through the tail entries
+  int64_t tail_roll = 0;              // > 0: the tail copy is refreshed chunk by chunk inside the epoch (every
+                                      // tail_roll-th row one 1024-float chunk) instead of between slices
   bool die_split = false;
   uint8_t *sm_die = nullptr;          // device [kMaxSm]: die of each SM id
   int n_die_sm[2] = {0, 0};

@@ -39,6 +39,8 @@ struct EpochArgs {
   const float *svr;  // head kernel with a tail read copy: gathers of ids >= H read svr (else == sv)
   const float *svg;  // gather source of the plain kernels: sv, or svr for a snapshot bin (Bin::snap)
   double lam, lamN;
+  int64_t roll_R;          // head kernel, rolling tail copy: every roll_R-th row refreshes one chunk (0 = off)
+  int64_t roll_lo, roll_hi;  // the tail range [roll_lo, roll_hi) kept in svr
 };
 
 struct BinArgs {
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
   __shared__ float s_red[NW];
   __shared__ float s_delta;
   __shared__ unsigned int s_ticket;
-  __shared__ int64_t s_cur[3];  // PF: coordinate (-1 = slice done), ptr[c], ptr[c + 1]
+  __shared__ int64_t s_cur[4];  // PF: coordinate (-1 = slice done), ptr[c], ptr[c + 1], its position t
   __shared__ float s_cx[3];     // PF: x[c], norm[c], y[c]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int i = tid; i < H; i += T) s_acc[i] = b.dry ? -0.f : 0.f;
@@ -369,11 +371,12 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
     __syncthreads();
     head_flush<T, true>(a.sv, s_acc, s_w, H, 0);  // initial view (nothing pending yet)
   }
-  int64_t n_c = -1, n_beg = 0, n_end = 0;  // PF (thread 0): the next coordinate
+  int64_t n_c = -1, n_beg = 0, n_end = 0, n_t = 0;  // PF (thread 0): the next coordinate
   float n_x = 0.f, n_nrm = 0.f, n_y = 0.f;
   unsigned n_tk = 0;
   auto fetch = [&](unsigned tk) {
     const int64_t t = b.lo + (int64_t)tk;
+    n_t = t;
     n_c = -1;
     if (t >= b.hi) return;
     n_c = bin_coord(b, t);
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
         s_cur[0] = n_c;
         s_cur[1] = n_beg;
         s_cur[2] = n_end;
+        s_cur[3] = n_t;
         s_cx[0] = n_x;
         s_cx[1] = n_nrm;
         s_cx[2] = n_y;
@@ -402,6 +406,19 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
       if (c < 0) break;
       beg = s_cur[1];
       end = s_cur[2];
+      if (TS && a.roll_R > 0 && !b.dry && s_cur[3] % a.roll_R == 0) {
+        // rolling tail copy: row position t refreshes chunk (t / roll_R) mod nchunks of
+        // svr from sv, so every tail entry of the copy is at most roll_R · nchunks positions old
+        // without any slice boundary (plain stores: a concurrent reader sees the old or the new value)
+        constexpr int64_t CH = (int64_t)T * 4;
+        const int64_t nch = (a.roll_hi - a.roll_lo + CH - 1) / CH;
+        const int64_t i = a.roll_lo + ((s_cur[3] / a.roll_R) % nch) * CH + (int64_t)tid * 4;
+        float *dst = const_cast<float *>(a.svr);
+        if (i + 3 < a.roll_hi)
+          *reinterpret_cast<float4 *>(dst + i) = __ldcg(reinterpret_cast<const float4 *>(a.sv + i));
+        else
+          for (int64_t q = i; q < a.roll_hi && q < i + 4; ++q) dst[q] = __ldcg(a.sv + q);
+      }
     } else {
       if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
       __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
@@ -1336,6 +1353,9 @@ EpochArgs make_args(scd_ctx *c) {
   a.sv = c->sv;
   a.svr = c->tail_snap ? c->svr : c->sv;
   a.svg = c->sv;
+  a.roll_R = c->tail_roll;
+  a.roll_lo = c->tail_lo;
+  a.roll_hi = c->tail_hi;
   a.lam = c->lam;
   a.lamN = c->lamN;
   return a;

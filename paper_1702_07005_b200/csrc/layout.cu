@@ -454,6 +454,23 @@ scd_status build_schedule(scd_ctx *c) {
       SCD_CK(c, cudaMalloc((void **)&c->svr, sizeof(float) * (size_t)c->n_shared));
       SCD_CK(c, cudaMemsetAsync(c->svr, 0, sizeof(float) * (size_t)c->n_shared, c->stream));
       S = 8;
+      // Rolling refresh (single head bin): the copy is refreshed 1024 floats at a time by every
+      // tail_roll-th row, so that one full sweep of the tail takes no more rows than a slice would
+      // (cap_fraction · τ_tail and 1/8 of the bin), and the epoch needs no slice boundaries (each
+      // costs a drain of the grid behind the longest rows: ~65 µs on C3).
+      // SCD_TAIL_ROLL=0: refresh between 8 slices instead.
+      c->tail_roll = 0;
+      const bool roll_env_off = getenv("SCD_TAIL_ROLL") && atoi(getenv("SCD_TAIL_ROLL")) == 0;
+      if (c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf) {
+        const Bin &B = c->bins[bi];
+        const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
+        const double sweep = std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0);
+        const int64_t R = nch > 0 ? (int64_t)(sweep / (double)nch) : 0;
+        if (R >= 1) {
+          c->tail_roll = R;
+          S = 1;
+        }
+      }
     } else {
       c->tail_snap = 0;
     }

@@ -49,3 +49,19 @@ for tune in ("1", "0"):
         print(f"tune={tune}: create {t1 - t0:.3f} s, offset {inf['sv_offset_bytes']}, probe {inf['probe_ms']}, "
               f"epoch {e0.elapsed_time(e1) / 4:.2f} ms", flush=True)
         s.close()
+# device-resident inputs: the create-time analysis alone (validation, norms, schedule, staleness
+# estimates, placement probe), with and without the tail-copy estimate and the probe
+dp, di, dv, dy = (x.cuda() for x in (hp, hi, hv, hy))
+for env in ({}, {"SCD_TAIL_SNAP": "0"}, {"SCD_SV_TUNE": "0"}, {"SCD_TAIL_SNAP": "0", "SCD_SV_TUNE": "0"}):
+    for k in ("SCD_TAIL_SNAP", "SCD_SV_TUNE"):
+        os.environ.pop(k, None)
+    os.environ.update(env)
+    ts = []
+    for rep in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s = scd.Solver(dp, di, dv, rows, cfg.n_cols, dy, cfg.lam, "dual", seed=3)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        s.close()
+    print(f"device inputs {env or 'default'}: create " + " ".join(f"{t:.3f}" for t in ts) + " s", flush=True)
