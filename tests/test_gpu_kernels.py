@@ -76,6 +76,11 @@ def test_head_kernel_schedule_and_convergence(c3p, monkeypatch):
     # tail read copy: only while one slice of the bin stays within half the tail coupling's bound
     if info["tail_snap"]:
         assert b["count"] / info["n_slices"] <= 0.5 * info["tail_tau"], info
+    # single head bin: the copy is refreshed in rolling chunks inside one launch per epoch; a full
+    # sweep (R rows per 1024-float chunk) stays within the same bounds as a slice
+    assert info["tail_snap"] == 1 and info["tail_roll"] >= 1 and info["n_slices"] == 1, info
+    nch = -(-(int(c3p[0]["idx"].max()) + 1 - b["head"]) // 1024)
+    assert info["tail_roll"] * nch <= min(0.5 * info["tail_tau"], b["count"] / 8), (info["tail_roll"], nch)
 
 
 def test_tail_read_copy_convergence(c3p, monkeypatch):
