@@ -389,14 +389,17 @@ def main():
                        "lambda": cfg.lam, "l2": "inputs larger than L2 (10.4 GB CSR per GPU, 126 MB L2)",
                        "parallelism": f"dp{world}" if world > 1 else "single GPU",
                        "schedule": bins, "inflight_cap": info["inflight_cap"], "tau_star": info["tau_star"],
-                       "tail_read_copy": bool(info.get("tail_snap")), "tail_tau": info.get("tail_tau")},
+                       "tail_read_copy": bool(info.get("tail_snap")), "tail_tau": info.get("tail_tau"),
+                       "tail_roll": info.get("tail_roll"), "n_slices": info.get("n_slices")},
             "time_to_gap_1e-4_s": (ttg or {}).get("seconds"), "time_to_gap": ttg,
             "hbm_gbs": (BYTES_PER_NNZ * total_nnz + BYTES_PER_COORD * rows * world) / (ms_step / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": f"{kname} (bin {b_i}, {bb['lanes']} lanes/coord"
                                    + (f", head {bb['head']} floats combined, flush every {bb['flush']}" if bb.get("head") else "")
-                                   + (", tail gathers from the per-slice read copy" if bb.get("head") and info.get("tail_snap") else "")
+                                   + ((", tail gathers from the read copy refreshed in rolling chunks (one launch per epoch)"
+                                       if info.get("tail_roll") else ", tail gathers from the per-slice read copy")
+                                      if bb.get("head") and info.get("tail_snap") else "")
                                    + ")",
                          "kernel_ms_avg": ms_b / cnt_b if cnt_b else None, "kernel_share_of_step": kernel_share,
                          "bytes_per_launch": bytes_launch, "peak_source": peak_src,
