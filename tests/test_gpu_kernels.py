@@ -240,3 +240,38 @@ def test_tail_read_copy_ragged_two_bins(monkeypatch):
     assert gaps[-1] <= 1e-5
     for t in (0, 1, 3):
         assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
+
+
+def test_schedule_rules_small_lambda():
+    """C3 prefix with λN = 35 (10x less regularisation than C3): every staleness bound shrinks, so the
+    schedule must shrink its windows / drop the read copies accordingly, and the iterates must still
+    reach the oracle's optimum inside the sequential band (DESIGN.md §6 rules, readings c25/c26)."""
+    d = synth.gen_host(synth.CONFIGS["C3"].with_rows(20_000))
+    pr = solver.Problem.from_csr(d, lam=35.0 / 20_000)
+    _, _, hist = solver.solve(pr, "dual", E, seed=4)
+    s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=4)
+    info = s.info()
+    print("schedule", info)
+    for b in info["bins"]:
+        inflight = b["grid"] * (b["block"] // b["lanes"] if b["lanes"] <= 32 else 1)
+        assert inflight <= b["cap"] + 1 or b["lanes"] > 256, b
+        if b["head"]:
+            assert b["grid"] * (1 + b["flush"]) <= b["tau"], b
+    if info["tail_snap"]:
+        sweep = info["tail_roll"] * -(-(int(d["idx"].max()) + 1 - 8192) // 1024) if info["tail_roll"] else \
+            max(b["count"] for b in info["bins"]) / info["n_slices"]
+        assert sweep <= 0.5 * info["tail_tau"] + 1, (sweep, info["tail_tau"])
+    gaps = []
+    for t in range(1, E + 1):
+        s.epoch(t)
+        gaps.append(s.duality_gap())
+    x = s.get_model().astype(np.float64)
+    s.close()
+    A = pr.A()
+    print("gpu gaps", ["%.2e" % g for g in gaps])
+    print("seq gaps", ["%.2e" % h["gap"] for h in hist])
+    Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+    assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
+    assert gaps[-1] <= 1e-5
+    for t in (0, 1, 3):
+        assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
