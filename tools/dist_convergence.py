@@ -44,15 +44,21 @@ def col_shards(p, i, v, owner, K):
     return out
 
 
+PARTS = int(os.environ.get("DIST_PARTS", "1"))  # > 1: sub-epoch rounds (scd_epoch_part)
+
+
 def run(solvers, mode, rounds, n_shared, stop=1e-6):
     recs = []
-    for r in range(1, rounds + 1):
+    for r in range(1, rounds * PARTS + 1):
         ms = []
         for s in solvers:
             st = torch.cuda.ExternalStream(s.stream_handle)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            s.epoch(r)
+            if PARTS > 1:
+                s.epoch_part((r - 1) // PARTS + 1, (r - 1) % PARTS, PARTS)
+            else:
+                s.epoch(r)
             e1.record(st)
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
@@ -80,7 +86,8 @@ def main():
         for K in [k for k in (1, 2, 4, 8) if k <= kmax]:
             owner = torch.from_numpy(scd.partition(4, cfg.n_cols, K).astype(np.int64)).cuda()
             shards = col_shards(p, i, v, owner, K)
-            for mode in ("add", "average", "optimal") if K > 1 else ("average",):
+            for mode in [m for m in (("add", "average", "optimal") if K > 1 else ("average",))
+                         if K == 1 or m in os.environ.get("DIST_MODES", "optimal,average,add")]:
                 solvers = [scd.Solver(sp, si, sv_, cfg.n_rows, nc, y, cfg.lam, "primal", seed=10 + k)
                            for k, (sp, si, sv_, nc) in enumerate(shards)]
                 recs = run(solvers, mode, rounds, cfg.n_rows)
@@ -102,7 +109,7 @@ def main():
             assert bool((d["val"] == 1).all())
             shards.append((d["ptr"], d["idx"], d["y"]))
             del d
-        for mode in ("optimal", "average", "add"):
+        for mode in [m for m in ("optimal", "average", "add") if m in os.environ.get("DIST_MODES", "optimal,average,add")]:
             solvers = [scd.Solver(sp, si, None, rows, cfg.n_cols, sy, cfg.lam, "dual", seed=10 + k,
                                   n_global=cfg.n_rows) for k, (sp, si, sy) in enumerate(shards)]
             recs = run(solvers, mode, rounds if mode != "add" else 4, cfg.n_cols, stop=1e-6)
@@ -114,7 +121,8 @@ def main():
             for s in solvers:
                 s.close()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    json.dump(results, open(os.path.join(ROOT, "gpurun_out", f"dist_{which}.json"), "w"), indent=1)
+    sfx = f"_parts{PARTS}" if PARTS > 1 else ""
+    json.dump(results, open(os.path.join(ROOT, "gpurun_out", f"dist_{which}{sfx}.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
