@@ -106,6 +106,23 @@ def c3_cfg(world: int):
     return base.with_rows(base.n_rows * world, name=f"C3x{world}" if world > 1 else "C3")
 
 
+def host_info() -> dict:
+    """The box's host (SURVEY §8(d) oracle timing protocol: nproc, CPU model, RAM)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["ram_gb"] = round(int(line.split()[1]) / 1e6, 1)
+                break
+    except OSError:
+        pass
+    return info
+
+
 def cpu_baseline(seconds: float = 15.0, rows: int = 20_000):
     """The fp64 oracle's dual epoch (Alg. 1 / Eq. 4, sequential, 1 core) on the first ``rows`` rows
     of C3; returns nnz/s over whole epochs within ~``seconds``."""
@@ -126,7 +143,7 @@ def cpu_baseline(seconds: float = 15.0, rows: int = 20_000):
         if time.perf_counter() - t0 >= seconds:
             break
     el = time.perf_counter() - t0
-    return {"value": done / el, "unit": "nnz/s", "cores": 1, "kind": "oracle",
+    return {"value": done / el, "unit": "nnz/s", "cores": 1, "kind": "oracle", "host": host_info(),
             "sample": f"C3 rows [0,{rows}) ({pr.nnz:.3g} nnz), {ep} sequential fp64 dual epochs (oracle.c, 1 thread)"}
 
 
@@ -156,7 +173,7 @@ def run_reference(args):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"C3 webspam-shaped dual TPA-SCD; reference arm = fp64 sequential oracle on a "
                                   f"bounded sample (rows [0,{rows}), {pr.nnz} nnz)", "form": "dual", "lambda": 1e-3},
-           "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": 1, "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": 1, "kind": "oracle", "host": host_info(),
                             "sample": f"C3 rows [0,{rows}) per step"},
            "e2e": {"value": v, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "note": "the paper ships no code; the reference arm is the sequential fp64 oracle (Alg. 1) on host cores"}
