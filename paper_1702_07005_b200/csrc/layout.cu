@@ -372,22 +372,10 @@ scd_status build_schedule(scd_ctx *c) {
     lim1 = 64;
     if (const char *e = getenv("SCD_HEAD_MIN")) lim1 = std::max<int64_t>(64, std::min<int64_t>(1024, atoll(e) - 1));
   }
-  const int64_t lim[NB] = {64, lim1, 16384, INT64_MAX};
-  std::vector<int32_t> lists[NB], empty;
-  int64_t nnzb[NB] = {0, 0, 0, 0};
-  for (int64_t i = 0; i < n; ++i) {
-    const int64_t L = hp[(size_t)i + 1] - hp[(size_t)i];
-    if (L == 0) {
-      empty.push_back((int32_t)i);
-      continue;
-    }
-    for (int b = 0; b < NB; ++b)
-      if (L <= lim[b]) {
-        lists[b].push_back((int32_t)i);
-        nnzb[b] += L;
-        break;
-      }
-  }
+  // empty coordinates (any lim1)
+  std::vector<int32_t> empty;
+  for (int64_t i = 0; i < n; ++i)
+    if (hp[(size_t)i + 1] == hp[(size_t)i]) empty.push_back((int32_t)i);
   c->n_empty = (int64_t)empty.size();
   c->n_nonempty = n - c->n_empty;
   if (c->n_empty) {
@@ -402,30 +390,61 @@ scd_status build_schedule(scd_ctx *c) {
   }
   if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
   c->head_pf = !(getenv("SCD_HEAD_PF") && atoi(getenv("SCD_HEAD_PF")) == 0);
-  // launch order: longest coordinates first
-  c->n_bins = 0;
-  c->tau_star = 1e18;
-  for (int b = NB - 1; b >= 0; --b) {
-    if (lists[b].empty()) continue;
-    Bin &B = c->bins[c->n_bins];
-    B.lanes = lanes[b];
-    B.count = (int64_t)lists[b].size();
-    B.nnz = nnzb[b];
-    B.stream_id = 1u + (uint32_t)c->n_bins;
-    if (B.count == n) {
-      B.list = nullptr;  // identity: every coordinate is in this bin
-    } else {
-      SCD_CK(c, cudaMalloc((void **)&B.list, sizeof(int32_t) * lists[b].size()));
-      SCD_CK(c, cudaMemcpy(B.list, lists[b].data(), sizeof(int32_t) * lists[b].size(), cudaMemcpyHostToDevice));
+  // one binning pass with the medium-row boundary lim1 (launch order: longest coordinates first)
+  auto bin_pass = [&](int64_t l1) -> scd_status {
+    const int64_t lim[NB] = {64, l1, 16384, INT64_MAX};
+    std::vector<int32_t> lists[NB];
+    int64_t nnzb[NB] = {0, 0, 0, 0};
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t L = hp[(size_t)i + 1] - hp[(size_t)i];
+      if (L == 0) continue;
+      for (int b = 0; b < NB; ++b)
+        if (L <= lim[b]) {
+          lists[b].push_back((int32_t)i);
+          nnzb[b] += L;
+          break;
+        }
     }
-    scd_status st = estimate_bin_tau(c, B.list, B.count, &B.tau);
-    if (st != SCD_OK) return st;
-    if (B.tau < c->tau_star) c->tau_star = B.tau;
-    double cap = cap_fraction() * B.tau;
-    B.cap = c->opt.max_inflight > 0 ? (int64_t)c->opt.max_inflight : (int64_t)(cap < 1 ? 1 : (cap > 1e9 ? 1e9 : cap));
-    B.head = B.lanes == kLanesCta ? head : 0;
-    bin_launch_shape(c, B);
-    ++c->n_bins;
+    c->n_bins = 0;
+    c->tau_star = 1e18;
+    for (int b = NB - 1; b >= 0; --b) {
+      if (lists[b].empty()) continue;
+      Bin &B = c->bins[c->n_bins];
+      B = Bin();
+      B.lanes = lanes[b];
+      B.count = (int64_t)lists[b].size();
+      B.nnz = nnzb[b];
+      B.stream_id = 1u + (uint32_t)c->n_bins;
+      if (B.count == n) {
+        B.list = nullptr;  // identity: every coordinate is in this bin
+      } else {
+        SCD_CK(c, cudaMalloc((void **)&B.list, sizeof(int32_t) * lists[b].size()));
+        SCD_CK(c, cudaMemcpy(B.list, lists[b].data(), sizeof(int32_t) * lists[b].size(), cudaMemcpyHostToDevice));
+      }
+      scd_status st = estimate_bin_tau(c, B.list, B.count, &B.tau);
+      if (st != SCD_OK) return st;
+      if (B.tau < c->tau_star) c->tau_star = B.tau;
+      double cap = cap_fraction() * B.tau;
+      B.cap = c->opt.max_inflight > 0 ? (int64_t)c->opt.max_inflight : (int64_t)(cap < 1 ? 1 : (cap > 1e9 ? 1e9 : cap));
+      B.head = B.lanes == kLanesCta ? head : 0;
+      bin_launch_shape(c, B);
+      ++c->n_bins;
+    }
+    return SCD_OK;
+  };
+  if (scd_status st = bin_pass(lim1); st != SCD_OK) return st;
+  if (lim1 < 1024) {
+    // the medium rows only belong in the CTA bin when its head-combining kernel is actually used
+    // (its window may not fit the staleness budget): otherwise bin again with the warp bin
+    bool head_used = false;
+    for (int i = 0; i < c->n_bins; ++i) head_used |= c->bins[i].lanes == kLanesCta && c->bins[i].head > 0;
+    if (!head_used) {
+      for (int i = 0; i < c->n_bins; ++i) {
+        cudaFree(c->bins[i].list);
+        c->bins[i] = Bin();
+      }
+      if (scd_status st = bin_pass(1024); st != SCD_OK) return st;
+    }
   }
   if (scd_status st = setup_hot(c); st != SCD_OK) return st;
   // interleave the bins in slices when more than one bin carries work (reading c24); SCD_SLICES overrides
