@@ -253,8 +253,9 @@ def test_schedule_rules_small_lambda():
     info = s.info()
     print("schedule", info)
     for b in info["bins"]:
-        inflight = b["grid"] * (b["block"] // b["lanes"] if b["lanes"] <= 32 else 1)
-        assert inflight <= b["cap"] + 1 or b["lanes"] > 256, b
+        per_cta = b["block"] // b["lanes"] if b["lanes"] <= 32 else 1
+        # the cap is honoured up to rounding to whole CTAs (bin_launch_shape)
+        assert b["grid"] * per_cta <= b["cap"] + per_cta or b["lanes"] > 256, b
         if b["head"]:
             assert b["grid"] * (1 + b["flush"]) <= b["tau"], b
     if info["tail_snap"]:
