@@ -86,6 +86,7 @@ constexpr int kLanesCluster = kClusterCtas * kClusterThreads;  // bin kind: one 
 struct Bin {
   int lanes = 0;             // lanes per coordinate: 8 / 32 (sub-warp group), 256 (CTA), 4096 (cluster)
   double tau = 0.0;          // estimated staleness bound of the bin (coordinates in flight)
+  double tau_tail = 0.0;     // head bin: bound of the coupling through the tail entries alone (0 = not estimated)
   int64_t cap = 0;           // coordinates in flight allowed
   int plain = 0;             // 1 = plain sub-warp kernel (cap below the combining kernel's CTA batch)
   int head = 0;              // CTA bins: > 0 = head-combining kernel over sv[0, head) (k_epoch_cta_head)
@@ -215,7 +216,8 @@ void set_global_error(const std::string &msg);
 scd_status validate_matrix(scd_ctx *c, int64_t outer, int64_t inner);
 scd_status compute_norms(scd_ctx *c);
 scd_status build_schedule(scd_ctx *c);
-scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau);
+scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau, int64_t lo = -1,
+                            double *tau_tail = nullptr);
 scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, int64_t lo, double *tau);
 scd_status renumber_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
                            int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, int32_t *new_of_old, cudaStream_t s,

@@ -285,22 +285,55 @@ static scd_status setup_tail_snap(scd_ctx *c, int head) {
 // coordinate-Hessian block), with d̄ = mean ||a||² and c̄ = mean |<a_i, a_j>| over pairs of the bin,
 // obtained from ||(|A_b|ᵀ1)||² = Σ_i Σ_j |<a_i,a_j>| (so c̄ upper-bounds the mean |<a_i,a_j>|).
 // Bins run one after another, so only intra-bin concurrency matters.
-scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau) {
+// One pass for both bounds (lo >= 0): the tail sums are the restriction of the same |A_b|ᵀ1 to
+// ids >= lo, plus the tail entries' own squares (acc[2]) — see estimate_tail_tau below.
+__global__ void k_abs_scatter2(const int64_t *ptr, const int32_t *idx, const float *val, const int32_t *list,
+                               int64_t count, const float *norm, int32_t lo, double *s, double *acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double sq = 0.0;
+  for (int64_t j = warp; j < count; j += nwarps) {
+    const int64_t o = list ? list[j] : j;
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) {
+      const int32_t i = idx[k];
+      const double v = (double)val_at(val, k);
+      atomicAdd(s + i, fabs(v));
+      if (i >= lo) sq += v * v;
+    }
+    if (lane == 0) atomicAdd(acc + 1, (double)norm[o]);
+  }
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0 && sq != 0.0) atomicAdd(acc + 2, sq);
+}
+
+scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau, int64_t lo,
+                            double *tau_tail) {
   cudaStream_t s = c->stream;
   double *vec = c->vec64;
   SCD_CK(c, cudaMemsetAsync(vec, 0, sizeof(double) * (size_t)c->n_shared, s));
-  SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 2, s));
-  k_abs_scatter<<<grid_for(count * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, d_list, count, c->norm, vec,
-                                                                    c->acc);
+  SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 8, s));
+  const bool tail = lo >= 0 && lo < c->n_shared && tau_tail;
+  if (tail)
+    k_abs_scatter2<<<grid_for(count * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, d_list, count, c->norm,
+                                                                       (int32_t)lo, vec, c->acc);
+  else
+    k_abs_scatter<<<grid_for(count * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, d_list, count, c->norm,
+                                                                      vec, c->acc);
   k_sumsq<<<grid_for(c->n_shared, 256, 148 * 8), 256, 0, s>>>(vec, c->n_shared, c->acc);
+  if (tail) k_sumsq<<<grid_for(c->n_shared - lo, 256, 148 * 8), 256, 0, s>>>(vec + lo, c->n_shared - lo, c->acc + 5);
   SCD_CKL(c, "coupling estimate");
-  double h[2];
+  double h[8];
   SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(h), cudaMemcpyDeviceToHost, s));
   SCD_CK(c, cudaStreamSynchronize(s));
   const double n = (double)(count > 1 ? count : 2);
   const double cbar = (h[0] - h[1]) / (n * (n - 1.0));
   const double dbar = h[1] / n + c->lamN;
   *tau = cbar > 0 ? dbar / cbar : 1e18;
+  if (tail) {
+    const double ct = (h[5] - h[2]) / (n * (n - 1.0));
+    *tau_tail = ct > 0 ? dbar / ct : 1e18;
+  }
   return SCD_OK;
 }
 
@@ -421,7 +454,9 @@ scd_status build_schedule(scd_ctx *c) {
         SCD_CK(c, cudaMalloc((void **)&B.list, sizeof(int32_t) * lists[b].size()));
         SCD_CK(c, cudaMemcpy(B.list, lists[b].data(), sizeof(int32_t) * lists[b].size(), cudaMemcpyHostToDevice));
       }
-      scd_status st = estimate_bin_tau(c, B.list, B.count, &B.tau);
+      // the CTA bin of the head kernel also gets its tail bound (tail read copy) from the same pass
+      const bool want_tail = c->tail_snap && B.lanes == kLanesCta && head > 0;
+      scd_status st = estimate_bin_tau(c, B.list, B.count, &B.tau, want_tail ? (int64_t)head : -1, &B.tau_tail);
       if (st != SCD_OK) return st;
       if (B.tau < c->tau_star) c->tau_star = B.tau;
       double cap = cap_fraction() * B.tau;
@@ -464,7 +499,10 @@ scd_status build_schedule(scd_ctx *c) {
     bool keep = bi >= 0;
     if (keep) {
       const Bin &B = c->bins[bi];
-      if (scd_status st = estimate_tail_tau(c, B.list, B.count, c->tail_lo, &c->tail_tau); st != SCD_OK) return st;
+      c->tail_tau = B.tau_tail;
+      if (!(c->tail_tau > 0)) {  // not estimated in the binning pass
+        if (scd_status st = estimate_tail_tau(c, B.list, B.count, c->tail_lo, &c->tail_tau); st != SCD_OK) return st;
+      }
       const double slice_rows = (double)B.count / (double)(S_env ? S_env : 8);
       const bool forced = getenv("SCD_TAIL_SNAP") != nullptr;
       keep = forced || (c->opt.max_inflight == 0 && slice_rows <= cap_fraction() * c->tail_tau);
