@@ -204,6 +204,8 @@ typedef struct {
                              before it (the slice's coordinates are within the bin's in-flight cap) */
   int64_t tail_roll;      /* > 0: the tail copy is refreshed inside the epoch, one 1024-float chunk every tail_roll
                              rows (no slice boundaries); 0 = refreshed between slices */
+  int64_t head_copy;      /* > 0: the head gathers also read a copy of w̄[0, bin_head) refreshed in rolling
+                             1024-float chunks every head_copy rows; 0 = off */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

@@ -485,6 +485,7 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->tail_snap = c->tail_snap;
   info->tail_tau = c->tail_tau;
   info->tail_roll = c->tail_roll;
+  info->head_copy = c->head_copy;
   info->inflight_cap = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i) {
     info->bin_cap[i] = c->bins[i].cap;

@@ -160,6 +160,7 @@ struct scd_ctx {
   bool hot_view = false;              // hot-set kernel also keeps a per-CTA view of the hot values
   double hot_cover = 0.0;             // share of the bin's entries that are hot
   bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)
+  int64_t head_copy = 0;              // experiment: head gathers from svr[0, H) refreshed every head_copy rows per chunk
   bool head_pf = true;                // head kernel prefetches the next coordinate (SCD_HEAD_PF=0: off)
   int tail_snap = 0;                  // head kernel reads the tail [tail_lo, tail_hi) of the shared vector from a
                                       // read copy refreshed before every slice: 1 = L2 loads, 2 = L1-cached loads
@@ -230,6 +231,7 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts);
 scd_status profile_collect(scd_ctx *c);
 scd_status tune_shared_layout(scd_ctx *c);
 void bin_launch_shape(scd_ctx *c, Bin &b);
+double combine_budget(const scd_ctx *c, const Bin &b);  // deferred-update budget of a bin (reading c25)
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
 scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);
 

@@ -40,6 +40,7 @@ struct EpochArgs {
   const float *svg;  // gather source of the plain kernels: sv, or svr for a snapshot bin (Bin::snap)
   double lam, lamN;
   int64_t roll_R;          // head kernel, rolling tail copy: every roll_R-th row refreshes one chunk (0 = off)
+  int64_t head_P;          // head kernel, head copy in svr[0, H): every head_P-th row refreshes one chunk (0 = off)
   int64_t roll_lo, roll_hi;  // the tail range [roll_lo, roll_hi) kept in svr
 };
 
@@ -354,7 +355,7 @@ __device__ __forceinline__ float ld_tail(const EpochArgs &a, int32_t j) {
 // ticket -> Feistel -> ptr -> x chain (three dependent round trips) leaves the per-row critical
 // path.  The prefetched coordinate reads nothing of the shared vector before its turn, so this adds
 // no staleness; x[c'] is current because this CTA is its only writer in the epoch (c10).
-template <int FORM, int T, int E, bool SNAP, int TS = 0, bool PF = false>
+template <int FORM, int T, int E, bool SNAP, int TS = 0, bool PF = false, bool HC = false>
 __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
   constexpr int NW = T / 32;
   extern __shared__ float4 s_dyn[];
@@ -406,6 +407,14 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
       if (c < 0) break;
       beg = s_cur[1];
       end = s_cur[2];
+      if (HC && !b.dry && s_cur[3] % a.head_P == 0) {
+        // head copy (experiment): row position t refreshes chunk (t / head_P) mod (H / 1024) of svr[0, H)
+        const int64_t nchh = ((int64_t)H + T * 4 - 1) / (T * 4);
+        const int64_t ih = ((s_cur[3] / a.head_P) % nchh) * (T * 4) + (int64_t)tid * 4;
+        if (ih + 3 < H)
+          *reinterpret_cast<float4 *>(const_cast<float *>(a.svr) + ih) =
+              __ldcg(reinterpret_cast<const float4 *>(a.sv + ih));
+      }
       if (TS && a.roll_R > 0 && !b.dry && s_cur[3] % a.roll_R == 0) {
         // rolling tail copy: row position t refreshes chunk (t / roll_R) mod nchunks of
         // svr from sv, so every tail entry of the copy is at most roll_R · nchunks positions old
@@ -449,7 +458,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
         if (SNAP)
           w = id[e] < H ? s_w[id[e]] + s_acc[id[e]] : ld_tail<TS>(a, id[e]);
         else if (TS)
-          w = id[e] < H ? ld_sv(a.sv + id[e]) + s_acc[id[e]] : ld_tail<TS>(a, id[e]);
+          w = id[e] < H ? ld_sv((HC ? a.svr : a.sv) + id[e]) + s_acc[id[e]] : ld_tail<TS>(a, id[e]);
         else
           w = ld_sv(a.sv + id[e]) + (id[e] < H ? s_acc[id[e]] : 0.f);
         acc = fmaf(w, v[e], acc);
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b,
           if (SNAP)
             w = j < H ? s_w[j] + s_acc[j] : ld_tail<TS>(a, j);
           else if (TS)
-            w = j < H ? ld_sv(a.sv + j) + s_acc[j] : ld_tail<TS>(a, j);
+            w = j < H ? ld_sv((HC ? a.svr : a.sv) + j) + s_acc[j] : ld_tail<TS>(a, j);
           else
             w = ld_sv(a.sv + j) + (j < H ? s_acc[j] : 0.f);
           acc = fmaf(w, val_cg(a.val, k), acc);
@@ -1328,6 +1337,8 @@ void *bin_kernel(const scd_ctx *c, const Bin &b) {
     return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true, 2>
                              : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true, 1>;
   if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && !c->head_snap && c->form == SCD_DUAL) {
+    if (c->head_pf && c->head_copy > 0 && c->tail_snap == 1)
+      return (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true, true>;
     if (c->head_pf)
       return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 2, true>
                                : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true>;
@@ -1354,6 +1365,7 @@ EpochArgs make_args(scd_ctx *c) {
   a.svr = c->tail_snap ? c->svr : c->sv;
   a.svg = c->sv;
   a.roll_R = c->tail_roll;
+  a.head_P = c->head_copy;
   a.roll_lo = c->tail_lo;
   a.roll_hi = c->tail_hi;
   a.lam = c->lam;
@@ -1385,10 +1397,14 @@ cudaEvent_t get_event(scd_ctx *c) {
 // 20 000-row C3 prefix a window of 5 rows per CTA (3 500 of 19 400 coordinates deferred) left the
 // gap 15x behind the sequential one after 4 epochs, so the deferred total is also kept <= 1/8 of the
 // bin's coordinates (never binding on the full-size configs).
-int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t k) {
+double combine_budget(const scd_ctx *c, const Bin &b) {
   const double frac = getenv("SCD_COMBINE_BUDGET") ? atof(getenv("SCD_COMBINE_BUDGET")) : 1.0;
-  double budget = c->opt.max_inflight > 0 ? (double)b.cap : frac * b.tau;
-  budget = std::min(budget, (double)b.count / 8.0);
+  const double budget = c->opt.max_inflight > 0 ? (double)b.cap : frac * b.tau;
+  return std::min(budget, (double)b.count / 8.0);
+}
+
+int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t k) {
+  const double budget = combine_budget(c, b);
   if (inflight < 1 || budget <= 0) return 0;
   return (int64_t)((budget / (double)inflight - 1.0) / (double)k);
 }
@@ -1596,7 +1612,7 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       if (grid > need) grid = need;
       if (grid < 1) grid = 1;
       if (c->tail_snap && b.head > 0 && b.lanes == kLanesCta) {
-        k_tail_refresh<<<c->nsm * 4, 256, 0, s>>>(c->sv, c->svr, c->tail_lo, c->tail_hi);
+        k_tail_refresh<<<c->nsm * 4, 256, 0, s>>>(c->sv, c->svr, c->head_copy > 0 ? 0 : c->tail_lo, c->tail_hi);
         SCD_CKL(c, "k_tail_refresh launch");
         ++c->launches;
       }

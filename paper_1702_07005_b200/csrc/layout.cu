@@ -423,6 +423,7 @@ scd_status build_schedule(scd_ctx *c) {
   }
   if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
   c->head_pf = !(getenv("SCD_HEAD_PF") && atoi(getenv("SCD_HEAD_PF")) == 0);
+  c->head_copy = 0;
   // one binning pass with the medium-row boundary lim1 (launch order: longest coordinates first)
   auto bin_pass = [&](int64_t l1) -> scd_status {
     const int64_t lim[NB] = {64, l1, 16384, INT64_MAX};
@@ -526,6 +527,29 @@ scd_status build_schedule(scd_ctx *c) {
         if (R >= 1) {
           c->tail_roll = R;
           S = 1;
+        }
+      }
+      // Head copy: the head gathers also read svr[0, H), refreshed in rolling 1024-float chunks every
+      // P rows, so they too land on lines that take no REDs.  A head read may then miss what was flushed
+      // in the last P · nchunks rows: that age joins the combined-update budget (reading c25),
+      // rows in flight + deferred + age = grid · (1 + flush) + P · nchunks <= budget; the flush window
+      // gives way (down to 2) until P >= 16 fits (a shorter period costs more in refresh traffic than
+      // it saves: profiles/head_copy_r1.txt).  SCD_HEAD_COPY=0: off, =P: forced period.
+      Bin &HB = c->bins[bi];
+      const char *hce = getenv("SCD_HEAD_COPY");
+      if (c->tail_roll > 0 && HB.head > 0 && !(hce && atoll(hce) == 0)) {
+        const int64_t nchh = (HB.head + 4 * kLanesCta - 1) / (4 * kLanesCta);
+        const double budget = combine_budget(c, HB);
+        int64_t P = 0;
+        int f = HB.flush;
+        for (; f >= 2; --f) {
+          P = (int64_t)((budget - (double)HB.grid * (1.0 + f)) / (double)nchh);
+          if (P >= 16) break;
+        }
+        if (hce) P = atoll(hce);
+        if (P >= 16 || hce) {
+          c->head_copy = std::max<int64_t>(1, P);
+          if (!hce) HB.flush = f;
         }
       }
     } else {

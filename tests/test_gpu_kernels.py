@@ -81,6 +81,10 @@ def test_head_kernel_schedule_and_convergence(c3p, monkeypatch):
     assert info["tail_snap"] == 1 and info["tail_roll"] >= 1 and info["n_slices"] == 1, info
     nch = -(-(int(c3p[0]["idx"].max()) + 1 - b["head"]) // 1024)
     assert info["tail_roll"] * nch <= min(0.5 * info["tail_tau"], b["count"] / 8), (info["tail_roll"], nch)
+    # head copy: rows in flight + deferred + the copy's age stay within the combined-update budget
+    if info["head_copy"]:
+        age = info["head_copy"] * -(-b["head"] // 1024)
+        assert info["head_copy"] >= 16 and b["grid"] * (1 + b["flush"]) + age <= min(b["tau"], b["count"] / 8), info
 
 
 def test_tail_read_copy_convergence(c3p, monkeypatch):
