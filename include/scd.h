@@ -206,6 +206,8 @@ typedef struct {
                              rows (no slice boundaries); 0 = refreshed between slices */
   int64_t head_copy;      /* > 0: the head gathers also read a copy of w̄[0, bin_head) refreshed in rolling
                              1024-float chunks every head_copy rows; 0 = off */
+  int64_t hot_copy;       /* > 0: the hot-set kernel gathers the hot values from a copy refreshed 32 slots at a
+                             time every hot_copy warp tickets; 0 = off */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

@@ -58,6 +58,7 @@ void free_ctx(scd_ctx *c) {
   cudaFree(c->sm_die);
   cudaFree(c->hot_idx);
   cudaFree(c->hot_ids);
+  cudaFree(c->hot_hc);
   cudaFree(c->split_mid);
   cudaFree(c->split_idx);
   cudaFree(c->split_val);
@@ -486,6 +487,7 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->tail_tau = c->tail_tau;
   info->tail_roll = c->tail_roll;
   info->head_copy = c->head_copy;
+  info->hot_copy = c->hot_copy;
   info->inflight_cap = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i) {
     info->bin_cap[i] = c->bins[i].cap;

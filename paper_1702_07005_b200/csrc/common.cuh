@@ -157,6 +157,8 @@ struct scd_ctx {
   // the ones whose shared-vector entry is homed in die 0's L2 come first
   int32_t *hot_idx = nullptr;         // device [nnz]: re-encoded indices for the hot-set kernel (hot.cu)
   int32_t *hot_ids = nullptr;         // device [K]: shared-vector index of each hot slot
+  int64_t hot_copy = 0;               // hot-set kernel: > 0 = hot values gathered from the rolling copy hot_hc (period)
+  float *hot_hc = nullptr;            // device [K]: rolling copy of the hot values in slot order
   bool hot_view = false;              // hot-set kernel also keeps a per-CTA view of the hot values
   double hot_cover = 0.0;             // share of the bin's entries that are hot
   bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)

@@ -979,9 +979,19 @@ struct HotArgs {
   const int32_t *hot_ids;  // [K]: shared-vector index of each hot slot
   int K;                   // hot slots (multiple of 4)
   int F;                   // row batches per warp between flushes
+  float *hc;               // HC: [K] rolling copy of the hot values (slot order), gathered instead of sv
+  int P;                   // HC: every P-th warp ticket refreshes 32 slots of hc
 };
 
-template <int FORM, int G, int E, bool VIEW>
+// hc[s] = sv[hot_ids[s]] for every slot (before each hot-bin launch when the copy is used)
+__global__ void k_hot_refresh(const float *sv, const int32_t *hot_ids, int K, float *hc) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) hc[i] = __ldcg(sv + hot_ids[i]);
+}
+
+// HC: the hot values are gathered from h.hc, a copy in slot order refreshed 32 slots at a time by the
+// warp whose ticket t has (t / rows per warp) mod P = 0, so the gathers leave the lines that take the
+// flush REDs; the copy's age (P · K/32 tickets) is counted in the window budget (hot_launch_shape).
+template <int FORM, int G, int E, bool VIEW, bool HC = false>
 __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
   constexpr int CPW = 32 / G;
   const unsigned FULL = 0xffffffffu;
@@ -1007,6 +1017,14 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
     if (lane == 0) t0 = atomicAdd(b.counter, (unsigned)CPW);
     t0 = __shfl_sync(FULL, t0, 0);
     if (b.lo + (int64_t)t0 >= b.hi) return -2;  // slice exhausted (uniform)
+    if (HC && !b.dry) {
+      const int64_t tk = (b.lo + (int64_t)t0) / CPW;
+      if (tk % h.P == 0) {
+        const int nch = (h.K + 31) / 32;
+        const int sl = (int)((tk / h.P) % nch) * 32 + lane;
+        if (sl < h.K) h.hc[sl] = __ldcg(a.sv + s_hid[sl]);
+      }
+    }
     int64_t cl = -1;
     if (lane < CPW && b.lo + (int64_t)t0 + lane < b.hi) cl = bin_coord(b, b.lo + t0 + lane);
     return __shfl_sync(FULL, cl, sub);
@@ -1064,7 +1082,7 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
             w[e] = ld_sv(a.sv + cur.id[e]);
           } else {
             const int sl = cur.id[e] & 0x7fffffff;
-            w[e] = (VIEW ? s_aux[sl] : ld_sv(a.sv + s_hid[sl])) + s_pend[sl];
+            w[e] = (VIEW ? s_aux[sl] : (HC ? __ldcg(h.hc + sl) : ld_sv(a.sv + s_hid[sl]))) + s_pend[sl];
           }
         }
       }
@@ -1319,6 +1337,9 @@ void *cluster_kernel(int cl) {
 }
 
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
+  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view)
+    return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true>
+                                 : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true>;
   if (b.hot > 0 && b.lanes == 8 && !c->opt.wild) {
     if (c->form == SCD_PRIMAL)
       return c->hot_view ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, true> : (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false>;
@@ -1440,6 +1461,30 @@ void hot_launch_shape(scd_ctx *c, Bin &b) {
   b.grid = (int)std::max<int64_t>(grid, 1);
   b.block = T;
   b.flush = (int)F;
+  // Hot copy: the copy's age, P · K/32 warp tickets of rows/warp rows each, joins the window budget:
+  // rows in flight · (1 + F) + age <= budget; F gives way (down to 4) until P >= 8 fits.
+  // SCD_HOT_COPY=0: off, =P: forced period.
+  c->hot_copy = 0;
+  const char *hce = getenv("SCD_HOT_COPY");
+  if (!c->hot_view && !(hce && atoll(hce) == 0) && T == 512) {
+    const double budget = combine_budget(c, b);
+    const int64_t inflight = (int64_t)b.grid * rows, nch = (b.hot + 31) / 32, cpw = 32 / 8;
+    int64_t P = 0, f = F;
+    for (; f >= 4; --f) {
+      P = (int64_t)((budget - (double)inflight * (1.0 + f)) / (double)(nch * cpw));
+      if (P >= 8) break;
+    }
+    if (hce) P = atoll(hce);
+    if (P >= 8 || hce) {
+      if (!c->hot_hc && cudaMalloc((void **)&c->hot_hc, sizeof(float) * (size_t)b.hot) != cudaSuccess) {
+        cudaGetLastError();
+        c->hot_hc = nullptr;
+        return;
+      }
+      c->hot_copy = std::max<int64_t>(1, P);
+      if (!hce) b.flush = (int)f;
+    }
+  }
 }
 
 // Grid/block for a bin (used by build_schedule): persistent, sized to the SM count times the
@@ -1535,6 +1580,8 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
     ha.hot_ids = c->hot_ids;
     ha.K = b.hot;
     ha.F = b.flush;
+    ha.hc = c->hot_hc;
+    ha.P = (int)std::max<int64_t>(1, c->hot_copy);
     args = args_hot;
   }
   if (b.split) {
@@ -1614,6 +1661,11 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       if (c->tail_snap && b.head > 0 && b.lanes == kLanesCta) {
         k_tail_refresh<<<c->nsm * 4, 256, 0, s>>>(c->sv, c->svr, c->head_copy > 0 ? 0 : c->tail_lo, c->tail_hi);
         SCD_CKL(c, "k_tail_refresh launch");
+        ++c->launches;
+      }
+      if (c->hot_copy > 0 && b.hot > 0 && b.lanes == 8) {
+        k_hot_refresh<<<grid_for(b.hot, 256), 256, 0, s>>>(c->sv, c->hot_ids, b.hot, c->hot_hc);
+        SCD_CKL(c, "k_hot_refresh launch");
         ++c->launches;
       }
       EpochArgs ab = a;
