@@ -519,7 +519,7 @@ scd_status build_schedule(scd_ctx *c) {
       // SCD_TAIL_ROLL=0: refresh between 8 slices instead.
       c->tail_roll = 0;
       const bool roll_env_off = getenv("SCD_TAIL_ROLL") && atoi(getenv("SCD_TAIL_ROLL")) == 0;
-      if (c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf) {
+      if (c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf && !c->head_snap) {
         const Bin &B = c->bins[bi];
         const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
         const double sweep = std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0);
