@@ -208,6 +208,9 @@ typedef struct {
                              1024-float chunks every head_copy rows; 0 = off */
   int64_t hot_copy;       /* > 0: the hot-set kernel gathers the hot values from a copy refreshed 32 slots at a
                              time every hot_copy warp tickets; 0 = off */
+  int32_t hot_tp;         /* 1: the hot-set kernel gathers the next batch's non-hot values one step early */
+  double hot_tail_tau;    /* staleness bound of the hot bin's coupling through its non-hot entries; the early
+                             gather is used only while 2 x rows in flight <= hot_tail_tau / 2 */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

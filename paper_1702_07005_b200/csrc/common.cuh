@@ -157,6 +157,8 @@ struct scd_ctx {
   // the ones whose shared-vector entry is homed in die 0's L2 come first
   int32_t *hot_idx = nullptr;         // device [nnz]: re-encoded indices for the hot-set kernel (hot.cu)
   int32_t *hot_ids = nullptr;         // device [K]: shared-vector index of each hot slot
+  bool hot_tp = false;                // hot-set kernel gathers the next batch's tail values one step early
+  double hot_tail_tau = 0.0;          // staleness bound of the hot bin's coupling through its non-hot entries
   int64_t hot_copy = 0;               // hot-set kernel: > 0 = hot values gathered from the rolling copy hot_hc (period)
   float *hot_hc = nullptr;            // device [K]: rolling copy of the hot values in slot order
   bool hot_view = false;              // hot-set kernel also keeps a per-CTA view of the hot values
@@ -221,7 +223,8 @@ scd_status compute_norms(scd_ctx *c);
 scd_status build_schedule(scd_ctx *c);
 scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, double *tau, int64_t lo = -1,
                             double *tau_tail = nullptr);
-scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, int64_t lo, double *tau);
+scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, int64_t lo, double *tau,
+                             const int32_t *idx = nullptr);
 scd_status renumber_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,
                            int64_t nnz, int64_t *optr, int32_t *oidx, float *oval, int32_t *new_of_old, cudaStream_t s,
                            std::string &err);
@@ -234,6 +237,7 @@ scd_status profile_collect(scd_ctx *c);
 scd_status tune_shared_layout(scd_ctx *c);
 void bin_launch_shape(scd_ctx *c, Bin &b);
 double combine_budget(const scd_ctx *c, const Bin &b);  // deferred-update budget of a bin (reading c25)
+double cap_fraction();  // in-flight cap as a fraction of a staleness bound (layout.cu)
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
 scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);
 

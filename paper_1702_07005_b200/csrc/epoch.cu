@@ -991,7 +991,7 @@ __global__ void k_hot_refresh(const float *sv, const int32_t *hot_ids, int K, fl
 // HC: the hot values are gathered from h.hc, a copy in slot order refreshed 32 slots at a time by the
 // warp whose ticket t has (t / rows per warp) mod P = 0, so the gathers leave the lines that take the
 // flush REDs; the copy's age (P · K/32 tickets) is counted in the window budget (hot_launch_shape).
-template <int FORM, int G, int E, bool VIEW, bool HC = false>
+template <int FORM, int G, int E, bool VIEW, bool HC = false, bool TP = false>
 __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
   constexpr int CPW = 32 / G;
   const unsigned FULL = 0xffffffffu;
@@ -1033,8 +1033,14 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
     int64_t c;
     int32_t id[E];
     float v[E];
+    float tw[E];  // TP: tail values gathered one step ahead
     unsigned valid;
     float xc, nrm, yc;
+  };
+  auto tail_prefetch = [&](Batch &q) {
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if ((q.valid >> e & 1) && q.id[e] >= 0) q.tw[e] = ld_sv(a.sv + q.id[e]);
   };
   auto load = [&](Batch &q, int64_t c) {
     q.c = c;
@@ -1066,6 +1072,7 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
   int64_t cn = take();
   bool more = cn != -2;  // warp-uniform: the warp holds a batch
   if (more) load(cur, cn);
+  if (TP && more) tail_prefetch(cur);
   for (;;) {
     for (int it = 0; it < h.F && more; ++it) {
       // next batch: ticket + coordinates + entries (no shared-vector access)
@@ -1079,7 +1086,7 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
         w[e] = 0.f;
         if (cur.valid >> e & 1) {
           if (cur.id[e] >= 0) {
-            w[e] = ld_sv(a.sv + cur.id[e]);
+            w[e] = TP ? cur.tw[e] : ld_sv(a.sv + cur.id[e]);
           } else {
             const int sl = cur.id[e] & 0x7fffffff;
             w[e] = (VIEW ? s_aux[sl] : (HC ? __ldcg(h.hc + sl) : ld_sv(a.sv + s_hid[sl]))) + s_pend[sl];
@@ -1109,7 +1116,10 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
           }
       }
       more = have_next;
-      if (have_next) cur = nxt;
+      if (have_next) {
+        cur = nxt;
+        if (TP) tail_prefetch(cur);  // the next batch's tail values, one step early
+      }
     }
     const bool any = __syncthreads_or(more);
     for (int i = threadIdx.x; i < h.K; i += blockDim.x) {  // flush (and refresh the view)
@@ -1337,6 +1347,9 @@ void *cluster_kernel(int cl) {
 }
 
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
+  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view && c->hot_tp)
+    return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true, true>
+                                 : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true, true>;
   if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view)
     return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true>
                                  : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true>;

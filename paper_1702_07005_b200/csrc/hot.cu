@@ -124,7 +124,20 @@ scd_status setup_hot(scd_ctx *c) {
   if (st != SCD_OK) return st;
   if (b.hot > 0) {
     c->hot_view = getenv("SCD_HOT_VIEW") && atoi(getenv("SCD_HOT_VIEW")) == 1;
+    // Tail prefetch: the next batch's non-hot values are gathered one step early, i.e. up to one more
+    // round of the rows in flight old.  Like the webspam tail copy (reading c26), that is allowed when
+    // the coupling through the non-hot entries alone bounds it: 2 x rows in flight <= cap_fraction x
+    // tau_tail (estimated from the re-encoded indices, hot entries excluded).  SCD_HOT_TP=0: off.
+    c->hot_tp = false;
+    if (!(getenv("SCD_HOT_TP") && atoi(getenv("SCD_HOT_TP")) == 0)) {
+      if (scd_status st2 = estimate_tail_tau(c, b.list, b.count, 0, &c->hot_tail_tau, c->hot_idx); st2 != SCD_OK)
+        return st2;
+    }
     bin_launch_shape(c, b);
+    if (b.hot > 0 && c->hot_tail_tau > 0) {
+      const double inflight = (double)b.grid * (b.block / 8);
+      c->hot_tp = 2.0 * inflight <= cap_fraction() * c->hot_tail_tau;
+    }
   }
   return SCD_OK;
 }

@@ -120,13 +120,6 @@ __global__ void __launch_bounds__(256) k_sumsq(const double *s, int64_t n, doubl
   block_sum_atomic<256>(a, acc + 0);
 }
 
-// Fraction of the estimated staleness bound used as the default in-flight cap (DESIGN.md §6);
-// SCD_CAP_FRACTION overrides it for tuning experiments (tools/sweep_inflight.py).
-double cap_fraction() {
-  const char *e = getenv("SCD_CAP_FRACTION");
-  double f = e ? atof(e) : 0.5;
-  return f > 0 ? f : 0.5;
-}
 
 // number of stored entries with inner index < H (sizing the head-combining kernel)
 __global__ void __launch_bounds__(256) k_count_below(const int32_t *idx, int64_t n, int32_t H, unsigned long long *out) {
@@ -162,6 +155,14 @@ __global__ void k_relabel(const int32_t *idx, int64_t n, const int32_t *new_of_o
 }
 
 }  // namespace
+
+// Fraction of the estimated staleness bound used as the default in-flight cap (DESIGN.md §6);
+// SCD_CAP_FRACTION overrides it for tuning experiments (tools/sweep_inflight.py).
+double cap_fraction() {
+  const char *e = getenv("SCD_CAP_FRACTION");
+  double f = e ? atof(e) : 0.5;
+  return f > 0 ? f : 0.5;
+}
 
 // Renumbering of the inner index space by frequency (SURVEY K8' "feature renumbering by frequency at
 // load"): new id = rank of the index by (occurrences descending, index ascending); entries relabelled
@@ -340,13 +341,16 @@ scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, do
 // Staleness bound of the bin's coupling through the shared-vector entries >= lo only (the tail read
 // copy of the head kernel): τ_tail = (λN + d̄) / c̄_tail, c̄_tail from ||(|A_b[:, lo:]|ᵀ1)||²
 // minus its diagonal terms.
-scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, int64_t lo, double *tau) {
+scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, int64_t lo, double *tau,
+                             const int32_t *idx) {
   cudaStream_t s = c->stream;
   double *vec = c->vec64;
   SCD_CK(c, cudaMemsetAsync(vec, 0, sizeof(double) * (size_t)c->n_shared, s));
   SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 3, s));
-  k_abs_scatter_tail<<<grid_for(count * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, c->idx, c->val, d_list, count, c->norm,
-                                                                         (int32_t)lo, vec, c->acc);
+  // idx: the entries to count (default the matrix's; the hot-set bin passes its re-encoded copy, whose
+  // hot entries are negative and so fall below lo = 0)
+  k_abs_scatter_tail<<<grid_for(count * 32, 256, 148 * 32), 256, 0, s>>>(c->ptr, idx ? idx : c->idx, c->val, d_list,
+                                                                         count, c->norm, (int32_t)lo, vec, c->acc);
   k_sumsq<<<grid_for(c->n_shared - lo, 256, 148 * 8), 256, 0, s>>>(vec + lo, c->n_shared - lo, c->acc);
   SCD_CKL(c, "tail coupling estimate");
   double h[3];

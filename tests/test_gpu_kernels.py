@@ -157,6 +157,8 @@ def test_hot_set_kernel_criteo_prefix(monkeypatch):
     print("schedule", info)
     assert b["lanes"] == 8 and b["hot"] > 0 and b["flush"] >= 4, b
     assert b["grid"] * (b["block"] // 8) * (1 + b["flush"]) <= b["tau"], b  # rows in flight + deferred
+    if info["hot_tp"]:  # early tail gathers: 2 x rows in flight within half the non-hot coupling bound
+        assert 2 * b["grid"] * (b["block"] // 8) <= 0.5 * info["hot_tail_tau"], info
     if info["hot_copy"]:  # + the age of the hot-value copy (P tickets per 32 slots, 4 rows per ticket)
         age = info["hot_copy"] * -(-b["hot"] // 32) * 4
         assert b["grid"] * (b["block"] // 8) * (1 + b["flush"]) + age <= b["tau"], (info["hot_copy"], b)
