@@ -211,6 +211,7 @@ typedef struct {
   int32_t hot_tp;         /* 1: the hot-set kernel gathers the next batch's non-hot values one step early */
   double hot_tail_tau;    /* staleness bound of the hot bin's coupling through its non-hot entries; the early
                              gather is used only while 2 x rows in flight <= hot_tail_tau / 2 */
+  int32_t hot_hp;         /* 1: the hot values of the next batch are also gathered one step early (from the copy) */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

@@ -489,6 +489,7 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->head_copy = c->head_copy;
   info->hot_copy = c->hot_copy;
   info->hot_tp = c->hot_tp ? 1 : 0;
+  info->hot_hp = (c->hot_hp && c->hot_copy > 0 && c->hot_tp) ? 1 : 0;
   info->hot_tail_tau = c->hot_tail_tau;
   info->inflight_cap = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i) {

@@ -157,6 +157,7 @@ struct scd_ctx {
   // the ones whose shared-vector entry is homed in die 0's L2 come first
   int32_t *hot_idx = nullptr;         // device [nnz]: re-encoded indices for the hot-set kernel (hot.cu)
   int32_t *hot_ids = nullptr;         // device [K]: shared-vector index of each hot slot
+  bool hot_hp = false;                // hot-set kernel also gathers the next batch's hot values (from the copy) early
   bool hot_tp = false;                // hot-set kernel gathers the next batch's tail values one step early
   double hot_tail_tau = 0.0;          // staleness bound of the hot bin's coupling through its non-hot entries
   int64_t hot_copy = 0;               // hot-set kernel: > 0 = hot values gathered from the rolling copy hot_hc (period)

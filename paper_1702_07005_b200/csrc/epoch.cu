@@ -991,7 +991,7 @@ __global__ void k_hot_refresh(const float *sv, const int32_t *hot_ids, int K, fl
 // HC: the hot values are gathered from h.hc, a copy in slot order refreshed 32 slots at a time by the
 // warp whose ticket t has (t / rows per warp) mod P = 0, so the gathers leave the lines that take the
 // flush REDs; the copy's age (P · K/32 tickets) is counted in the window budget (hot_launch_shape).
-template <int FORM, int G, int E, bool VIEW, bool HC = false, bool TP = false>
+template <int FORM, int G, int E, bool VIEW, bool HC = false, bool TP = false, bool HP = false>
 __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
   constexpr int CPW = 32 / G;
   const unsigned FULL = 0xffffffffu;
@@ -1040,7 +1040,12 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
   auto tail_prefetch = [&](Batch &q) {
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      if ((q.valid >> e & 1) && q.id[e] >= 0) q.tw[e] = ld_sv(a.sv + q.id[e]);
+      if (q.valid >> e & 1) {
+        if (q.id[e] >= 0)
+          q.tw[e] = ld_sv(a.sv + q.id[e]);
+        else if (HP)
+          q.tw[e] = __ldcg(h.hc + (q.id[e] & 0x7fffffff));  // HP: hot copy value one step early too
+      }
   };
   auto load = [&](Batch &q, int64_t c) {
     q.c = c;
@@ -1089,7 +1094,7 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
             w[e] = TP ? cur.tw[e] : ld_sv(a.sv + cur.id[e]);
           } else {
             const int sl = cur.id[e] & 0x7fffffff;
-            w[e] = (VIEW ? s_aux[sl] : (HC ? __ldcg(h.hc + sl) : ld_sv(a.sv + s_hid[sl]))) + s_pend[sl];
+            w[e] = (VIEW ? s_aux[sl] : (HP ? cur.tw[e] : (HC ? __ldcg(h.hc + sl) : ld_sv(a.sv + s_hid[sl])))) + s_pend[sl];
           }
         }
       }
@@ -1347,6 +1352,9 @@ void *cluster_kernel(int cl) {
 }
 
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
+  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view && c->hot_tp && c->hot_hp)
+    return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true, true, true>
+                                 : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true, true, true>;
   if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view && c->hot_tp)
     return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true, true>
                                  : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true, true>;
@@ -1475,16 +1483,19 @@ void hot_launch_shape(scd_ctx *c, Bin &b) {
   b.block = T;
   b.flush = (int)F;
   // Hot copy: the copy's age, P · K/32 warp tickets of rows/warp rows each, joins the window budget:
-  // rows in flight · (1 + F) + age <= budget; F gives way (down to 4) until P >= 8 fits.
-  // SCD_HOT_COPY=0: off, =P: forced period.
+  // rows in flight · (1 + F + hp) + age <= budget, hp = 1 when the hot values are also gathered one
+  // step early (hot_hp: one more round of the rows in flight); F gives way (down to 4) until P >= 8
+  // fits.  SCD_HOT_COPY=0: off, =P: forced period; SCD_HOT_HP=0: no early hot gathers.
   c->hot_copy = 0;
+  c->hot_hp = !(getenv("SCD_HOT_HP") && atoi(getenv("SCD_HOT_HP")) == 0);
   const char *hce = getenv("SCD_HOT_COPY");
   if (!c->hot_view && !(hce && atoll(hce) == 0) && T == 512) {
     const double budget = combine_budget(c, b);
     const int64_t inflight = (int64_t)b.grid * rows, nch = (b.hot + 31) / 32, cpw = 32 / 8;
+    const double hp = c->hot_hp ? 1.0 : 0.0;
     int64_t P = 0, f = F;
     for (; f >= 4; --f) {
-      P = (int64_t)((budget - (double)inflight * (1.0 + f)) / (double)(nch * cpw));
+      P = (int64_t)((budget - (double)inflight * (1.0 + hp + f)) / (double)(nch * cpw));
       if (P >= 8) break;
     }
     if (hce) P = atoll(hce);

@@ -49,7 +49,7 @@ class Info(C.Structure):
                 ("sv_offset_bytes", C.c_int64), ("probe_best_ms", C.c_float), ("probe_worst_ms", C.c_float),
                 ("bin_head", C.c_int32 * 4), ("bin_flush", C.c_int32 * 4), ("bin_split", C.c_int32 * 4),
                 ("die_split", C.c_int32), ("n_die_sm", C.c_int32 * 2), ("die_lat", C.c_float * 2), ("split_nnz0", C.c_int64), ("bin_hot", C.c_int32 * 4),
-                ("hot_cover", C.c_double), ("tail_snap", C.c_int32), ("tail_tau", C.c_double), ("bin_snap", C.c_int32 * 4), ("tail_roll", C.c_int64), ("head_copy", C.c_int64), ("hot_copy", C.c_int64), ("hot_tp", C.c_int32), ("hot_tail_tau", C.c_double)]
+                ("hot_cover", C.c_double), ("tail_snap", C.c_int32), ("tail_tau", C.c_double), ("bin_snap", C.c_int32 * 4), ("tail_roll", C.c_int64), ("head_copy", C.c_int64), ("hot_copy", C.c_int64), ("hot_tp", C.c_int32), ("hot_tail_tau", C.c_double), ("hot_hp", C.c_int32)]
 
 
 _lib = None
@@ -236,7 +236,7 @@ class Solver:
                     probe_ms=(inf.probe_best_ms, inf.probe_worst_ms), die_split=bool(inf.die_split),
                     n_die_sm=(inf.n_die_sm[0], inf.n_die_sm[1]), die_lat=(inf.die_lat[0], inf.die_lat[1]),
                     split_nnz0=inf.split_nnz0, hot_cover=inf.hot_cover, tail_snap=inf.tail_snap,
-                    tail_tau=inf.tail_tau, tail_roll=inf.tail_roll, head_copy=inf.head_copy, hot_copy=inf.hot_copy, hot_tp=inf.hot_tp, hot_tail_tau=inf.hot_tail_tau,
+                    tail_tau=inf.tail_tau, tail_roll=inf.tail_roll, head_copy=inf.head_copy, hot_copy=inf.hot_copy, hot_tp=inf.hot_tp, hot_tail_tau=inf.hot_tail_tau, hot_hp=inf.hot_hp,
                     bins=[dict(lanes=inf.bin_kind[i], count=inf.bin_count[i], nnz=inf.bin_nnz[i],
                                grid=inf.bin_grid[i], block=inf.bin_block[i], cap=inf.bin_cap[i],
                                tau=inf.bin_tau[i], head=inf.bin_head[i], flush=inf.bin_flush[i],

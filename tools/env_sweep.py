@@ -47,6 +47,6 @@ for st in settings:
         gaps.append(s.duality_gap())
     b0 = max(inf["bins"], key=lambda b: b["nnz"])
     print(f"[{st or 'default'}] bin lanes={b0['lanes']} grid={b0['grid']} cap={b0['cap']} hot={b0.get('hot', 0)} "
-          f"flush={b0['flush']} tail_snap={inf.get('tail_snap')} tail_tau={inf.get('tail_tau', 0):.0f} slices={inf['n_slices']} roll={inf.get('tail_roll', 0)} hcopy={inf.get('head_copy', 0)} hotcopy={inf.get('hot_copy', 0)} tp={inf.get('hot_tp', 0)} httau={inf.get('hot_tail_tau', 0):.3g}: epoch {ms:.2f} ms  gaps " + " ".join(f"{g:.2e}" for g in gaps)
+          f"flush={b0['flush']} tail_snap={inf.get('tail_snap')} tail_tau={inf.get('tail_tau', 0):.0f} slices={inf['n_slices']} roll={inf.get('tail_roll', 0)} hcopy={inf.get('head_copy', 0)} hotcopy={inf.get('hot_copy', 0)} tp={inf.get('hot_tp', 0)} hp={inf.get('hot_hp', 0)} httau={inf.get('hot_tail_tau', 0):.3g}: epoch {ms:.2f} ms  gaps " + " ".join(f"{g:.2e}" for g in gaps)
           + "  snap " + ",".join(f"{b['lanes']}:{b.get('snap', 0)}" for b in inf["bins"]), flush=True)
     s.close()
