@@ -510,7 +510,14 @@ scd_status build_schedule(scd_ctx *c) {
       }
       const double slice_rows = (double)B.count / (double)(S_env ? S_env : 8);
       const bool forced = getenv("SCD_TAIL_SNAP") != nullptr;
-      keep = forced || (c->opt.max_inflight == 0 && slice_rows <= cap_fraction() * c->tail_tau);
+      // either refreshed between slices (a slice within the bound) or, with one head bin, in rolling
+      // chunks whose full sweep is within the bound (possible with a shorter sweep than a slice)
+      const bool roll_env_off = getenv("SCD_TAIL_ROLL") && atoi(getenv("SCD_TAIL_ROLL")) == 0;
+      const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
+      const bool can_roll = c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf &&
+                            !c->head_snap && nch > 0 &&
+                            std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0) >= (double)nch;
+      keep = forced || (c->opt.max_inflight == 0 && (slice_rows <= cap_fraction() * c->tail_tau || can_roll));
     }
     if (keep) {
       SCD_CK(c, cudaMalloc((void **)&c->svr, sizeof(float) * (size_t)c->n_shared));
@@ -523,7 +530,8 @@ scd_status build_schedule(scd_ctx *c) {
       // SCD_TAIL_ROLL=0: refresh between 8 slices instead.
       c->tail_roll = 0;
       const bool roll_env_off = getenv("SCD_TAIL_ROLL") && atoi(getenv("SCD_TAIL_ROLL")) == 0;
-      if (c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf && !c->head_snap) {
+      if (c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf && !c->head_snap &&
+          c->opt.max_inflight == 0) {
         const Bin &B = c->bins[bi];
         const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
         const double sweep = std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0);
