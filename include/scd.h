@@ -70,16 +70,38 @@ typedef struct {
   scd_mem mem;
 } scd_matrix;
 
+/* Collective transport for world > 1.  The default is NCCL (scd_options.nccl_comm, over NVLink /
+ * NVSwitch).  Alternatively the caller may supply these two host-side hooks over its own process
+ * group (e.g. torch.distributed / gloo): NCCL refuses two ranks on one GPU, so the hooks are what
+ * lets the library's multi-rank logic (aggregation rounds, the active-extent exchange, the fused
+ * peer-memory exchange, the collective objective/gap, the shared-vector rebuild) run with several
+ * processes on a single device.  Both hooks receive DEVICE pointers of the calling context and
+ * its stream; they must complete the operation in the stream's order (e.g. synchronise the
+ * stream, reduce through host memory, copy back) before returning, and return 0 on success
+ * (anything else makes the library call fail with SCD_E_NCCL).
+ *   allreduce: in place, count elements of dtype (scd_dtype), op (scd_redop), every rank
+ *   allgather: recv[r*bytes, (r+1)*bytes) = rank r's send[0, bytes)
+ * The struct is BORROWED for the lifetime of the context.                                    */
+typedef enum { SCD_DT_F32 = 0, SCD_DT_F64 = 1, SCD_DT_I32 = 2, SCD_DT_I64 = 3, SCD_DT_U8 = 4 } scd_dtype;
+typedef enum { SCD_OP_SUM = 0, SCD_OP_MAX = 1, SCD_OP_MIN = 2 } scd_redop;
+typedef struct {
+  void *user;
+  int32_t (*allreduce)(void *user, void *buf, int64_t count, int32_t dtype, int32_t op, void *stream);
+  int32_t (*allgather)(void *user, const void *send, void *recv, int64_t bytes, void *stream);
+} scd_collectives;
+
 typedef struct {
   uint64_t seed;          /* permutation key: epoch t visits coordinates in P_t = feistel(seed, t) order (c8) */
   int64_t n_global;       /* N used in λN when the dual is sharded by example (c14); 0 = n_rows */
   int32_t rank, world;    /* world = K workers; 1 = single GPU (default) */
-  void *nccl_comm;        /* ncclComm_t, required iff world > 1 (see scd_nccl_comm_init); not owned */
+  void *nccl_comm;        /* ncclComm_t; world > 1 needs this or `collectives` (see scd_nccl_comm_init); not owned */
   void *stream;           /* cudaStream_t for all work; NULL = a context-owned stream */
   int32_t deterministic;  /* 1 = debug mode: ONE coordinate at a time in exact P_t order, fixed reduction
                              tree; bitwise repeatable (parity with the sequential oracle, Alg. 1) */
   int32_t max_inflight;   /* cap on coordinates in flight in the asynchronous kernels; 0 = auto */
-  int32_t recompute_every;/* rebuild the shared vector from the model every k epochs; 0 = off */
+  int32_t recompute_every;/* rebuild the shared vector from the model in fp64 (P:164 recomputation, SURVEY
+                             NEXT-2): world = 1 every k epochs (in scd_epoch); world > 1 every k rounds, at
+                             the end of scd_aggregate from the aggregated model (collective).  0 = off */
   int32_t validate;       /* 1 = check the matrix invariants on the device at create (default 1) */
   int32_t profile;        /* 1 = time every kernel launch of scd_epoch with CUDA events (scd_profile_read) */
   int32_t wild;           /* 1 = "wild" scatter: plain load + store instead of the atomic add, so concurrent
@@ -87,6 +109,7 @@ typedef struct {
                              SURVEY NEXT-4).  A measured comparison only: it converges to a point that
                              violates the optimality conditions.  Uses the plain kernels (no head
                              combining, no CTA combining).  0 = atomic (default, the paper's TPA-SCD). */
+  const scd_collectives *collectives; /* host-side transport hooks instead of nccl_comm (NULL = NCCL) */
 } scd_options;
 
 typedef struct scd_ctx scd_ctx;
@@ -104,7 +127,8 @@ void scd_default_options(scd_options *opt);
  * Initial state: model = 0, shared vector = 0 (w = Aβ = 0; w̄ = Aᵀα = 0), as in Alg. 1/2
  * "Initialize: β = 0, w = 0".  Precomputes the squared norms ||a_m||² / ||ā_n||²
  * (c9) and the coordinate schedule.  Errors: SCD_E_INVALID_ARG, SCD_E_BAD_MATRIX, SCD_E_OOM,
- * SCD_E_CUDA, SCD_E_STATE (world > 1 without nccl_comm).  On error *out is NULL.            */
+ * SCD_E_CUDA, SCD_E_STATE (world > 1 without nccl_comm or collectives), SCD_E_INVALID_ARG
+ * (dual with world > 1 and n_global = 0).  On error *out is NULL.                           */
 scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double lambda, scd_form form,
                       const scd_options *opt, scd_ctx **out);
 
@@ -223,7 +247,8 @@ scd_status scd_profile_read(scd_ctx *c, double *ms_out, int64_t *count_out, int3
 const char *scd_last_error(const scd_ctx *c);   /* context-owned, valid until the next call on c */
 const char *scd_last_global_error(void);         /* thread-local, for context-free calls */
 const char *scd_status_string(scd_status s);
-/* ABI check for bindings: sizes_out[0..2] = sizeof(scd_matrix), sizeof(scd_options), sizeof(scd_info). */
+/* ABI check for bindings: sizes_out[0..3] = sizeof(scd_matrix), sizeof(scd_options), sizeof(scd_info),
+ * sizeof(scd_collectives). */
 void scd_struct_sizes(int64_t *sizes_out);
 void scd_destroy(scd_ctx *c);                    /* NULL-safe; syncs the stream; frees owned memory */
 

@@ -30,8 +30,6 @@ def lib():
         L.orc_sq_norms.argtypes = [_I64, _P, _P, _P]
         L.orc_primal_epoch.argtypes = [_I64, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P, _I64, _P]
         L.orc_dual_epoch.argtypes = [_P, _P, _P, _P, _D, _I64, _P, _P, _P, _P, _I64, _P]
-        L.orc_spmv_gather.argtypes = [_I64, _P, _P, _P, _P, _P]
-        L.orc_spmv_scatter.argtypes = [_I64, _P, _P, _P, _P, _P]
         _lib = L
     return _lib
 

@@ -167,20 +167,3 @@ void orc_dual_epoch(const int64_t *rptr, const int32_t *cidx, const float *val, 
     }
   }
 }
-
-/* Sparse products used by the objective oracle (definitions, sequential, fp64):
- * out[o] = Σ_e val[e] x[idx[e]]  over outer o   (CSR: A x ; CSC: Aᵀ x) */
-void orc_spmv_gather(int64_t n_outer, const int64_t *ptr, const int32_t *idx, const float *val, const double *x,
-                     double *out) {
-  for (int64_t o = 0; o < n_outer; ++o) {
-    double s = 0.0;
-    for (int64_t e = ptr[o]; e < ptr[o + 1]; ++e) s += (double)val[e] * x[idx[e]];
-    out[o] = s;
-  }
-}
-/* out[idx[e]] += val[e] x[o]  (CSR: Aᵀ x ; CSC: A x); out must be zeroed by the caller. */
-void orc_spmv_scatter(int64_t n_outer, const int64_t *ptr, const int32_t *idx, const float *val, const double *x,
-                      double *out) {
-  for (int64_t o = 0; o < n_outer; ++o)
-    for (int64_t e = ptr[o]; e < ptr[o + 1]; ++e) out[idx[e]] += (double)val[e] * x[o];
-}

@@ -90,6 +90,35 @@ def gap_dual_gradform(A, y, lam, alpha) -> float:
     return float(g @ g / (2.0 * A.shape[0]))
 
 
+def dual_report(A, y, lam, alpha) -> tuple[float, float, float]:
+    """(P(Aᵀα/λ), D(α), G_D(α)) with the two sparse products shared (large problems):
+    v = Aᵀα, q = Av;  P = ||q/λ - y||²/(2N) + ||v||²/(2λ)  (Eq. 1 at β = v/λ, Eq. 5),
+    D = -N/2||α||² - ||v||²/(2λ) + αᵀy  (Eq. 3),  G_D = ||y - Nα - q/λ||²/(2N)  (c13).
+    Pinned equal to primal_objective / dual_objective / gap_dual_gradform."""
+    N = A.shape[0]
+    v = A.T @ alpha
+    q = A @ v
+    vv = float(v @ v)
+    r = q / lam - y
+    g = y - N * alpha - q / lam
+    return (float(r @ r) / (2.0 * N) + vv / (2.0 * lam), float(-0.5 * N * (alpha @ alpha) - vv / (2.0 * lam) + alpha @ y),
+            float(g @ g) / (2.0 * N))
+
+
+def primal_report(A, y, lam, beta) -> tuple[float, float, float]:
+    """(P(β), D((y - Aβ)/N), G_P(β)) with the two sparse products shared:
+    res = y - Aβ, g = Aᵀres;  P = ||res||²/(2N) + λ/2||β||²  (Eq. 1),
+    D(α̂ = res/N) = -||res||²/(2N) - ||g||²/(2λN²) + yᵀres/N  (Eq. 3, Eq. 6),
+    G_P = ||λβ - g/N||²/(2λ)  (c13).  Pinned equal to the separate functions."""
+    N = A.shape[0]
+    res = y - A @ beta
+    g = A.T @ res
+    rr = float(res @ res)
+    gr = lam * beta - g / N
+    return (rr / (2.0 * N) + 0.5 * lam * float(beta @ beta),
+            -rr / (2.0 * N) - float(g @ g) / (2.0 * lam * N * N) + float(y @ res) / N, float(gr @ gr) / (2.0 * lam))
+
+
 def closed_form(A, y, lam, cap: int = 4096) -> np.ndarray:
     """β* = argmin P = (AᵀA + λN I)⁻¹ Aᵀy  (zero of the gradient P:83; dense solve, M <= cap)."""
     N, M = A.shape

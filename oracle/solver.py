@@ -30,11 +30,15 @@ class Problem:
     cval: np.ndarray = field(default=None)
 
     @staticmethod
-    def from_csr(d: dict, lam: float | None = None) -> "Problem":
+    def from_csr(d: dict, lam: float | None = None, csc: bool = True) -> "Problem":
+        """d["val"] = None: implicit values (one-hot data, P:460 footnote) stored explicitly as 1.0.
+        csc=False skips the CSC copy (dual-only use: row norms and Eq. (4) epochs need only CSR)."""
+        val = d["val"] if d["val"] is not None else np.ones(len(d["idx"]), np.float32)
         pr = Problem(int(d["n_rows"]), int(d["n_cols"]), np.ascontiguousarray(d["ptr"], np.int64),
-                     np.ascontiguousarray(d["idx"], np.int32), np.ascontiguousarray(d["val"], np.float32),
+                     np.ascontiguousarray(d["idx"], np.int32), np.ascontiguousarray(val, np.float32),
                      np.asarray(d["y"], np.float32).astype(np.float64), float(d["lam"] if lam is None else lam))
-        pr.cptr, pr.cidx, pr.cval = transpose(pr.rptr, pr.ridx, pr.rval, pr.n_cols)
+        if csc:
+            pr.cptr, pr.cidx, pr.cval = transpose(pr.rptr, pr.ridx, pr.rval, pr.n_cols)
         return pr
 
     @property
@@ -95,9 +99,8 @@ def solve(pr: Problem, form: str, epochs: int, seed: int, first_epoch: int = 1, 
         for t in range(first_epoch, first_epoch + epochs):
             primal_epoch(pr, x, s, permutation(seed, t, pr.M), nrm)
             if record:
-                P = ridge.primal_objective(A, pr.y, pr.lam, x)
-                D = ridge.dual_objective(A, pr.y, pr.lam, ridge.primal_to_dual(A, pr.y, x))
-                hist.append(dict(epoch=t, P=P, D=D, gap=ridge.gap_primal_gradform(A, pr.y, pr.lam, x)))
+                P, D, G = ridge.primal_report(A, pr.y, pr.lam, x)
+                hist.append(dict(epoch=t, P=P, D=D, gap=G))
     elif form == "dual":
         x = np.zeros(pr.N)
         s = np.zeros(pr.M)
@@ -105,9 +108,8 @@ def solve(pr: Problem, form: str, epochs: int, seed: int, first_epoch: int = 1, 
         for t in range(first_epoch, first_epoch + epochs):
             dual_epoch(pr, x, s, permutation(seed, t, pr.N), nrm)
             if record:
-                P = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
-                D = ridge.dual_objective(A, pr.y, pr.lam, x)
-                hist.append(dict(epoch=t, P=P, D=D, gap=ridge.gap_dual_gradform(A, pr.y, pr.lam, x)))
+                P, D, G = ridge.dual_report(A, pr.y, pr.lam, x)
+                hist.append(dict(epoch=t, P=P, D=D, gap=G))
     else:
         raise ValueError(form)
     return x, s, hist
@@ -170,13 +172,6 @@ def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed
         s0 = s0 + g * ds
         x0 = x0 + g * dx
         if record:
-            if form == "primal":
-                P = ridge.primal_objective(A, pr.y, pr.lam, x0)
-                D = ridge.dual_objective(A, pr.y, pr.lam, ridge.primal_to_dual(A, pr.y, x0))
-                gap = ridge.gap_primal_gradform(A, pr.y, pr.lam, x0)
-            else:
-                P = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x0))
-                D = ridge.dual_objective(A, pr.y, pr.lam, x0)
-                gap = ridge.gap_dual_gradform(A, pr.y, pr.lam, x0)
+            P, D, gap = (ridge.primal_report if form == "primal" else ridge.dual_report)(A, pr.y, pr.lam, x0)
             hist.append(dict(epoch=t, gamma=g, P=P, D=D, gap=gap))
     return x0, s0, hist

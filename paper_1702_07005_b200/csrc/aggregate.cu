@@ -12,6 +12,12 @@
 //     dual   (denominator read as N||Δα||² (c4)):
 //             γ̄ = (S_ydx - N S_x0dx - <Δw̄, w̄₀>/λ) / (||Δw̄||²/λ + N S_dxdx)
 //     zero denominator -> γ = 0 (c16)
+//   The numerator's shared-vector term is taken at the base point from the coordinates, not from the
+//   fp32 vector delta: Δw = Σ_k A_k Δx_k, so <r₀, Δr> = -Σ_m Δβ_m <a_m, r₀> and <Δw̄, w̄₀> =
+//   Σ_n Δα_n <ā_n, w̄₀> (k_base_dot, fp64, one gather pass over the local matrix).  Near the optimum
+//   the two terms of the numerator nearly cancel (<r₀, Δr> ≈ -λN<β₀, Δβ> when ∇P(β₀) ≈ 0), and the
+//   vector delta carries the rounding of every fp32 RED of the epoch at the scale of |r| (~1e-6 per
+//   entry on C4), which then dominated the difference and made γ erratic below gap ~1e-5.
 //   sv = sv₀ + γΔ ;  x_k = x₀_k + γΔx_k ;  the result becomes the next base point (c6).
 //
 // Two implementations of the exchange:
@@ -67,6 +73,25 @@ __global__ void __launch_bounds__(kT) k_shared_dots(const float *sv0, const floa
   block_sum_atomic<kT>(b, acc + 4);
 }
 
+// acc[5] += Σ_c (x_c - x0_c) <a_c, sv0>: the base-point term of the optimal γ (fp64, warp per coordinate).
+// primal: sv0 = r₀ and the term is -<r₀, Δr>; dual: sv0 = w̄₀ and the term is <Δw̄, w̄₀>.
+__global__ void __launch_bounds__(kT) k_base_dot(const int64_t *ptr, const int32_t *idx, const float *val,
+                                                 const float *x, const float *x0, const float *sv0, int64_t n,
+                                                 double *acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double s = 0.0;
+  for (int64_t o = warp; o < n; o += nwarps) {
+    const double dx = (double)x[o] - (double)x0[o];
+    if (dx == 0.0) continue;  // warp-uniform
+    double c = 0.0;
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) c += (double)val_at(val, k) * (double)sv0[idx[k]];
+    s += dx * c;  // lanes' partials; summed below
+  }
+  block_sum_atomic<kT>(s, acc + 5);
+}
+
 __global__ void k_gamma(double *acc, int mode, int form, double K, double lam, double N) {
   double g;
   if (mode == SCD_AGG_ADD) {
@@ -76,11 +101,12 @@ __global__ void k_gamma(double *acc, int mode, int form, double K, double lam, d
   } else {
     const double lamN = lam * N;
     double num, den;
+    // acc[5] = Σ Δx_c <a_c, sv0> replaces <sv0, Δ> (acc[3]) in the numerator (see the header)
     if (form == SCD_PRIMAL) {
-      num = -(acc[3] + lamN * acc[0]);
+      num = -(-acc[5] + lamN * acc[0]);
       den = acc[4] + lamN * acc[1];
     } else {
-      num = acc[2] - N * acc[0] - acc[3] / lam;
+      num = acc[2] - N * acc[0] - acc[5] / lam;
       den = acc[4] / lam + N * acc[1];
     }
     g = den != 0.0 ? num / den : 0.0;
@@ -161,7 +187,7 @@ scd_status p2p_setup(scd_ctx *c) {
   IpcRec *d_all = nullptr;
   SCD_CK(c, cudaMalloc((void **)&d_all, sizeof(IpcRec) * (size_t)(K + 1)));
   SCD_CK(c, cudaMemcpyAsync(d_all + K, &mine, sizeof(IpcRec), cudaMemcpyHostToDevice, c->stream));
-  SCD_NCK(c, ncclAllGather(d_all + K, d_all, sizeof(IpcRec), ncclUint8, c->nccl, c->stream));
+  SCD_COLL(coll_allgather(c, d_all + K, d_all, sizeof(IpcRec)));
   std::vector<IpcRec> all((size_t)K);
   SCD_CK(c, cudaMemcpyAsync(all.data(), d_all, sizeof(IpcRec) * (size_t)K, cudaMemcpyDeviceToHost, c->stream));
   SCD_CK(c, cudaStreamSynchronize(c->stream));
@@ -189,7 +215,7 @@ scd_status p2p_setup(scd_ctx *c) {
   int32_t h_ok = ok ? 1 : 0;
   SCD_CK(c, cudaMalloc((void **)&d_ok, sizeof(int32_t)));
   SCD_CK(c, cudaMemcpyAsync(d_ok, &h_ok, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-  SCD_NCK(c, ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->nccl, c->stream));
+  SCD_COLL(coll_allreduce(c, d_ok, 1, SCD_DT_I32, SCD_OP_MIN));
   SCD_CK(c, cudaMemcpyAsync(&h_ok, d_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   SCD_CK(c, cudaStreamSynchronize(c->stream));
   cudaFree(d_ok);
@@ -220,15 +246,18 @@ static scd_status aggregate_p2p(scd_ctx *c, scd_agg mode, double *gamma) {
   float **peer = c->p2p_ptrs;
   SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 16, s));
   k_model_dots<<<grid_for(nc, kT), kT, 0, s>>>(c->x, c->x0, c->y, nc, dual, c->acc);
-  SCD_NCK(c, ncclAllReduce(c->acc, c->acc, 3, ncclDouble, ncclSum, c->nccl, s));
+  if (mode == SCD_AGG_OPTIMAL)
+    k_base_dot<<<grid_for(nc * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->x0, c->sv0, nc, c->acc);
+  SCD_COLL(coll_allreduce(c, c->acc, 6, SCD_DT_F64, SCD_OP_SUM));  // acc[3..4] are still 0 here
   k_agg_reduce<<<grid_for(hi - lo, kT), kT, 0, s>>>(peer, K, c->sv0, lo, hi, c->comm, c->acc);
-  SCD_NCK(c, ncclAllReduce(c->acc + 3, c->acc + 3, 2, ncclDouble, ncclSum, c->nccl, s));
+  SCD_COLL(coll_allreduce(c, c->acc + 3, 2, SCD_DT_F64, SCD_OP_SUM));
   k_gamma<<<1, 1, 0, s>>>(c->acc, (int)mode, (int)c->form, (double)K, c->lam, (double)c->n_global);
   k_agg_apply<<<grid_for(hi - lo, kT), kT, 0, s>>>(peer, peer + K, K, c->sv0, c->comm, lo, hi, c->acc);
-  SCD_NCK(c, ncclAllReduce(c->acc + 9, c->acc + 9, 1, ncclDouble, ncclSum, c->nccl, s));
+  SCD_COLL(coll_allreduce(c, c->acc + 9, 1, SCD_DT_F64, SCD_OP_SUM));
   k_apply_model<<<grid_for(nc, kT), kT, 0, s>>>(c->x, c->x0, nc, c->acc);
   SCD_CKL(c, "aggregate (fused peer exchange)");
-  c->launches += 5;
+  c->launches += 5 + (mode == SCD_AGG_OPTIMAL ? 1 : 0);
+  c->empty_dirty = true;  // x₀ + γΔx moved the empty coordinates off their fixed point (c17)
   double g = 0.0;
   SCD_CK(c, cudaMemcpyAsync(&g, c->acc + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
   SCD_CK(c, cudaStreamSynchronize(s));
@@ -238,7 +267,7 @@ static scd_status aggregate_p2p(scd_ctx *c, scd_agg mode, double *gamma) {
 
 scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
   // (a 1-rank communicator runs the same fused path: IPC export, handle all-gather, barriers)
-  if (c->nccl && getenv("SCD_P2P_AGG") && atoi(getenv("SCD_P2P_AGG")) == 1) {
+  if (c->has_comm() && getenv("SCD_P2P_AGG") && atoi(getenv("SCD_P2P_AGG")) == 1) {
     if (c->p2p_state == 0) {
       scd_status st = p2p_setup(c);
       if (st != SCD_OK) return st;
@@ -250,11 +279,11 @@ scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
   // the dual's w̄ is zero beyond the largest inner index of every rank's shard, so Δ is too: the
   // round exchanges [0, sv_active) only (exact; C3: 680 715 of 16.6 M entries), the extent being the
   // max over the ranks, reduced once
-  if (dual && c->nccl && c->opt.world > 1 && !c->sv_active_global) {
+  if (dual && c->has_comm() && c->opt.world > 1 && !c->sv_active_global) {
     int64_t *d = nullptr, h = c->sv_active;
     SCD_CK(c, cudaMallocAsync((void **)&d, sizeof(int64_t), s));
     SCD_CK(c, cudaMemcpyAsync(d, &h, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    SCD_NCK(c, ncclAllReduce(d, d, 1, ncclInt64, ncclMax, c->nccl, s));
+    SCD_COLL(coll_allreduce(c, d, 1, SCD_DT_I64, SCD_OP_MAX));
     SCD_CK(c, cudaMemcpyAsync(&h, d, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SCD_CK(c, cudaStreamSynchronize(s));
     cudaFreeAsync(d, s);
@@ -264,15 +293,19 @@ scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
   const int64_t ns = (dual && c->sv_active > 0) ? c->sv_active : c->n_shared, nc = c->n_coord;
   SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 16, s));
   k_model_dots<<<grid_for(nc, kT), kT, 0, s>>>(c->x, c->x0, c->y, nc, dual, c->acc);
+  if (mode == SCD_AGG_OPTIMAL) {
+    k_base_dot<<<grid_for(nc * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->x0, c->sv0, nc, c->acc);
+    ++c->launches;
+  }
   k_delta<<<grid_for(ns, kT), kT, 0, s>>>(c->sv, c->sv0, ns, 1, c->comm);
   SCD_CKL(c, "aggregate pack");
   c->launches += 2;
-  if (c->nccl) {  // collective whenever a communicator is attached (world = 1 exercises the same path)
+  if (c->has_comm()) {  // collective whenever a communicator is attached (world = 1 exercises the same path)
     // Σ_k Δw_k (Alg. 3/4 "Aggregate updates") and the worker scalars
-    SCD_NCK(c, ncclGroupStart());
-    SCD_NCK(c, ncclAllReduce(c->comm, c->comm, (size_t)ns, ncclFloat, ncclSum, c->nccl, s));
-    SCD_NCK(c, ncclAllReduce(c->acc, c->acc, 3, ncclDouble, ncclSum, c->nccl, s));
-    SCD_NCK(c, ncclGroupEnd());
+    SCD_COLL(coll_group_start(c));
+    SCD_COLL(coll_allreduce(c, c->comm, (size_t)ns, SCD_DT_F32, SCD_OP_SUM));
+    SCD_COLL(coll_allreduce(c, c->acc, 6, SCD_DT_F64, SCD_OP_SUM));  // acc[3..4] are still 0 here
+    SCD_COLL(coll_group_end(c));
   }
   k_shared_dots<<<grid_for(ns, kT), kT, 0, s>>>(c->sv0, c->comm, ns, c->acc);
   k_gamma<<<1, 1, 0, s>>>(c->acc, (int)mode, (int)c->form, (double)c->opt.world, c->lam, (double)c->n_global);
@@ -280,6 +313,7 @@ scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
   k_apply_model<<<grid_for(nc, kT), kT, 0, s>>>(c->x, c->x0, nc, c->acc);
   SCD_CKL(c, "aggregate apply");
   c->launches += 4;
+  c->empty_dirty = true;  // x₀ + γΔx moved the empty coordinates off their fixed point (c17)
   double g = 0.0;
   SCD_CK(c, cudaMemcpyAsync(&g, c->acc + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
   SCD_CK(c, cudaStreamSynchronize(s));
@@ -307,6 +341,11 @@ scd_status aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, double *
   for (int i = 0; i < k; ++i) {
     scd_ctx *c = cs[i];
     k_model_dots<<<grid_for(c->n_coord, kT), kT, 0, s>>>(c->x, c->x0, c->y, c->n_coord, dual, c0->acc);
+    if (mode == SCD_AGG_OPTIMAL) {  // each worker's coordinates against the common base point
+      k_base_dot<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->x0, c0->sv0,
+                                                                         c->n_coord, c0->acc);
+      c->launches += 1;
+    }
     c->launches += 1;
   }
   k_agg_reduce<<<grid_for(ns, kT), kT, 0, s>>>(d_ptrs, k, c0->sv0, 0, ns, c0->comm, c0->acc);
@@ -317,6 +356,7 @@ scd_status aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, double *
     scd_ctx *c = cs[i];
     k_apply_model<<<grid_for(c->n_coord, kT), kT, 0, s>>>(c->x, c->x0, c->n_coord, c0->acc);
     c->launches += 1;
+    c->empty_dirty = true;  // x₀ + γΔx moved the empty coordinates off their fixed point (c17)
   }
   SCD_CKL(c0, "aggregate_group kernels");
   cudaFreeAsync(d_ptrs, s);

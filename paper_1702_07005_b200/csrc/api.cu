@@ -174,6 +174,7 @@ void scd_struct_sizes(int64_t *sizes_out) {
   sizes_out[0] = (int64_t)sizeof(scd_matrix);
   sizes_out[1] = (int64_t)sizeof(scd_options);
   sizes_out[2] = (int64_t)sizeof(scd_info);
+  sizes_out[3] = (int64_t)sizeof(scd_collectives);
 }
 
 const char *scd_status_string(scd_status s) {
@@ -210,8 +211,15 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
   scd_default_options(&opt);
   if (opt_in) opt = *opt_in;
   if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(nullptr, SCD_E_INVALID_ARG, "bad rank/world");
-  if (opt.world > 1 && !opt.nccl_comm) return fail(nullptr, SCD_E_STATE, "world > 1 requires nccl_comm");
+  if (opt.world > 1 && !opt.nccl_comm && !opt.collectives)
+    return fail(nullptr, SCD_E_STATE, "world > 1 requires nccl_comm or collectives");
+  if (opt.collectives && (!opt.collectives->allreduce || !opt.collectives->allgather))
+    return fail(nullptr, SCD_E_INVALID_ARG, "collectives needs both allreduce and allgather");
   if (opt.n_global < 0) return fail(nullptr, SCD_E_INVALID_ARG, "n_global < 0");
+  // a dual shard needs the global N of λN (c14): a silent fallback to the local row count would
+  // change the coordinate update, γ and the objectives
+  if (form == SCD_DUAL && opt.world > 1 && opt.n_global == 0)
+    return fail(nullptr, SCD_E_INVALID_ARG, "dual with world > 1 needs n_global (global N)");
 
   scd_ctx *c = new (std::nothrow) scd_ctx();
   if (!c) return fail(nullptr, SCD_E_OOM, "host allocation failed");
@@ -226,6 +234,7 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
   c->n_global = form == SCD_PRIMAL ? A->n_rows : (opt.n_global > 0 ? opt.n_global : A->n_rows);
   c->lamN = lambda * (double)c->n_global;
   c->nccl = (ncclComm_t)opt.nccl_comm;
+  c->coll = c->nccl ? nullptr : opt.collectives;
   cudaGetDevice(&c->device);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
   scd_status st = SCD_OK;
@@ -299,6 +308,15 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
   cudaMemsetAsync(c->x0, 0, sizeof(float) * (size_t)c->n_coord, s);
   if ((st = compute_norms(c)) != SCD_OK) return bail(st);
   if ((st = build_schedule(c)) != SCD_OK) return bail(st);
+  if (!opt.validate) {
+    // the head and hot-set kernels accumulate a row's updates with plain shared-memory
+    // read-modify-writes, correct only for unique indices within a coordinate: with validation
+    // off, still check the index invariants whenever one of them was selected
+    bool combining = false;
+    for (int i = 0; i < c->n_bins; ++i) combining |= c->bins[i].head > 0 || c->bins[i].hot > 0;
+    const int64_t inner = form == SCD_PRIMAL ? c->n_rows : c->n_cols;
+    if (combining && (st = validate_matrix(c, outer, inner)) != SCD_OK) return bail(st);
+  }
   {
     // shared-vector placement: SCD_SV_OFFSET (bytes) pins it; otherwise large asynchronous
     // problems are probed (tune_shared_layout); SCD_SV_TUNE=0 disables the probe
@@ -337,6 +355,7 @@ scd_status scd_epoch_part(scd_ctx *c, uint32_t epoch, int32_t part, int32_t npar
   CK_CTX(c);
   if (nparts < 1 || part < 0 || part >= nparts || nparts > 1024)
     return fail(c, SCD_E_INVALID_ARG, "need 0 <= part < nparts <= 1024");
+  ++c->model_version;
   return run_epoch(c, epoch, part, nparts);
 }
 
@@ -345,9 +364,11 @@ scd_status scd_epoch(scd_ctx *c, uint32_t epoch) {
   scd_status st = run_epoch(c, epoch, 0, 1);
   if (st != SCD_OK) return st;
   ++c->epochs_done;
-  if (c->opt.recompute_every > 0 && (c->epochs_done % (uint32_t)c->opt.recompute_every) == 0) {
-    // P:164 recomputation scheme (single worker; resets the aggregation base point)
-    if (c->nccl) return fail(c, SCD_E_UNSUPPORTED, "recompute_every with world > 1: call scd_recompute_shared after scd_aggregate");
+  ++c->model_version;
+  // P:164 recomputation scheme.  Without a communicator it runs here, every k epochs;
+  // with one (world > 1) the shared vector is the sum over the ranks, so it is rebuilt from the
+  // aggregated model at the end of scd_aggregate (every k rounds) instead.
+  if (c->opt.recompute_every > 0 && !c->has_comm() && (c->epochs_done % (uint32_t)c->opt.recompute_every) == 0) {
     st = rebuild_shared(c);
     if (st != SCD_OK) return st;
   }
@@ -371,9 +392,19 @@ scd_status scd_aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
   CK_CTX(c);
   if (mode != SCD_AGG_ADD && mode != SCD_AGG_AVERAGE && mode != SCD_AGG_OPTIMAL)
     return fail(c, SCD_E_INVALID_ARG, "bad aggregation mode");
-  if (c->opt.world > 1 && !c->nccl) return fail(c, SCD_E_STATE, "no communicator");
+  if (c->opt.world > 1 && !c->has_comm()) return fail(c, SCD_E_STATE, "no communicator");
   if (scd_status st = check_split_error(c); st != SCD_OK) return st;
-  return aggregate(c, mode, gamma);
+  scd_status st = aggregate(c, mode, gamma);
+  if (st != SCD_OK) return st;
+  ++c->model_version;
+  ++c->rounds_done;
+  if (c->opt.recompute_every > 0 && c->has_comm() && (c->rounds_done % (uint32_t)c->opt.recompute_every) == 0) {
+    // rebuild the shared vector from the aggregated model: Σ_k A_k x_k in fp64 over the ranks
+    st = rebuild_shared(c);
+    if (st != SCD_OK) return st;
+    SCD_CK(c, cudaStreamSynchronize(c->stream));
+  }
+  return SCD_OK;
 }
 
 scd_status scd_aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, double *gamma) {
@@ -386,8 +417,11 @@ scd_status scd_aggregate_group(scd_ctx *const *cs, int32_t k, scd_agg mode, doub
     if (cs[i]->form != cs[0]->form || cs[i]->n_shared != cs[0]->n_shared || cs[i]->lam != cs[0]->lam ||
         cs[i]->device != cs[0]->device || cs[i]->n_global != cs[0]->n_global || cs[i]->opt.world != 1)
       return fail(nullptr, SCD_E_INVALID_ARG, "group contexts must share form, shared length, lambda, N, device; world = 1");
+    if (cs[i]->opt.recompute_every > 0)
+      return fail(nullptr, SCD_E_UNSUPPORTED, "recompute_every with logical workers (each would rebuild its own shard)");
   }
   scd_status st = aggregate_group(cs, k, mode, gamma);
+  for (int i = 0; i < k && st == SCD_OK; ++i) ++cs[i]->model_version;
   if (st != SCD_OK) g_err = cs[0]->err;
   return st;
 }
@@ -398,7 +432,7 @@ scd_status scd_evaluate_group(scd_ctx *const *cs, int32_t k, double *primal, dou
   for (int i = 0; i < k; ++i) {
     if (!cs[i]) return fail(nullptr, SCD_E_INVALID_ARG, "NULL context");
     if (cs[i]->form != cs[0]->form || cs[i]->n_shared != cs[0]->n_shared || cs[i]->lam != cs[0]->lam ||
-        cs[i]->device != cs[0]->device || cs[i]->n_global != cs[0]->n_global || cs[i]->nccl)
+        cs[i]->device != cs[0]->device || cs[i]->n_global != cs[0]->n_global || cs[i]->has_comm())
       return fail(nullptr, SCD_E_INVALID_ARG, "group contexts must share form, shared length, lambda, N, device; no comm");
   }
   scd_status st = evaluate_group(cs, k, primal, dual, gap);
@@ -428,6 +462,7 @@ scd_status scd_set_model(scd_ctx *c, const float *host_in, int64_t len) {
   CK_CTX(c);
   if (!host_in || len != c->n_coord) return fail(c, SCD_E_INVALID_ARG, "model length mismatch");
   SCD_CK(c, cudaMemcpyAsync(c->x, host_in, sizeof(float) * (size_t)len, cudaMemcpyHostToDevice, c->stream));
+  ++c->model_version;
   scd_status st = rebuild_shared(c);
   if (st != SCD_OK) return st;
   c->empty_dirty = true;

@@ -144,6 +144,11 @@ struct scd_ctx {
   double *vec64 = nullptr;  // [n_shared] fp64 (u = Aβ or v = Aᵀα)
   float *comm = nullptr;    // [n_shared] fp32 aggregation buffer (Δ of the shared vector)
   ncclComm_t nccl = nullptr;
+  const scd_collectives *coll = nullptr;  // host-side transport hooks (scd_options.collectives), instead of NCCL
+  bool has_comm() const { return nccl != nullptr || coll != nullptr; }
+  uint64_t model_version = 1;         // bumped by every change of the model (epoch, aggregation, set_model)
+  uint64_t vec64_version = 0;         // model_version vec64 = A x (fp64, all-reduced) was computed for
+  uint32_t rounds_done = 0;           // aggregation rounds (recompute_every with world > 1)
   int p2p_state = 0;                  // fused peer-memory aggregation: 0 = not set up, 1 = ready, -1 = unavailable
   float **p2p_ptrs = nullptr;         // device [2 * world]: every rank's sv, then every rank's sv0
   std::vector<void *> p2p_open;       // IPC mappings to close at destroy
@@ -210,6 +215,18 @@ void set_global_error(const std::string &msg);
   do {                                                     \
     cudaError_t e_ = cudaGetLastError();                   \
     if (e_ != cudaSuccess) return scd::cuda_fail(ctx, e_, what); \
+  } while (0)
+
+// collectives over the context's communicator: NCCL, or the caller's hooks (comm.cu).  All are
+// stream-ordered on c->stream; with the hooks they complete before returning.
+scd_status coll_allreduce(scd_ctx *c, void *buf, size_t count, scd_dtype dt, scd_redop op);
+scd_status coll_allgather(scd_ctx *c, const void *send, void *recv, size_t bytes);
+scd_status coll_group_start(scd_ctx *c);
+scd_status coll_group_end(scd_ctx *c);
+#define SCD_COLL(call)                   \
+  do {                                   \
+    scd_status st_ = (call);             \
+    if (st_ != SCD_OK) return st_;       \
   } while (0)
 
 #define SCD_NCK(ctx, call)                                 \

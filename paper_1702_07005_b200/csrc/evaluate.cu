@@ -29,12 +29,12 @@ __global__ void k_scatter64(const int64_t *ptr, const int32_t *idx, const float 
   }
 }
 
-// primal rows: res_i = y_i - u_i (stored in u), acc[0] += res², acc[1] += y·res
-__global__ void __launch_bounds__(kT) k_primal_rows(const float *y, double *u, int64_t n, double *acc) {
+// primal rows: res_i = y_i - u_i, acc[0] += res², acc[1] += y·res  (u = Aβ is kept: the shared-vector
+// rebuild may reuse it, see shared64)
+__global__ void __launch_bounds__(kT) k_primal_rows(const float *y, const double *u, int64_t n, double *acc) {
   double s_rr = 0.0, s_yr = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double r = (double)y[i] - u[i];
-    u[i] = r;
     s_rr += r * r;
     s_yr += (double)y[i] * r;
   }
@@ -42,17 +42,20 @@ __global__ void __launch_bounds__(kT) k_primal_rows(const float *y, double *u, i
   block_sum_atomic<kT>(s_yr, acc + 1);
 }
 
-// primal columns: g_m = <a_m, res>; acc[2] += (λβ_m - g_m/N)², acc[3] += β_m², acc[4] += g_m²
+// primal columns: g_m = <a_m, res>, res = y - u; acc[2] += (λβ_m - g_m/N)², acc[3] += β_m², acc[4] += g_m²
 __global__ void __launch_bounds__(kT) k_primal_cols(const int64_t *ptr, const int32_t *idx, const float *val,
-                                                    const float *beta, const double *res, int64_t outer, double lam,
-                                                    double N, double *acc) {
+                                                    const float *beta, const float *y, const double *u, int64_t outer,
+                                                    double lam, double N, double *acc) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double s_gg = 0.0, s_bb = 0.0, s_g2 = 0.0;
   for (int64_t o = warp; o < outer; o += nwarps) {
     double g = 0.0;
-    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) g += (double)val_at(val, k) * res[idx[k]];
+    for (int64_t k = ptr[o] + lane; k < ptr[o + 1]; k += 32) {
+      const int32_t i = idx[k];
+      g += (double)val_at(val, k) * ((double)y[i] - u[i]);
+    }
     g = warp_sum(g);
     if (lane == 0) {
       const double b = beta[o];
@@ -118,16 +121,20 @@ __global__ void k_w_from_r(const float *y, const float *r, int64_t n, float *w) 
 
 }  // namespace
 
-// u = A x (primal: Aβ over N rows) or v = Aᵀx (dual: over M cols) into c->vec64, summed over ranks.
+// u = A x (primal: Aβ over N rows) or v = Aᵀx (dual: over M cols) into c->vec64, summed over ranks
+// (collective).  The gap pass and the shared-vector rebuild (NEXT-2) both start from it, so
+// the scatter runs once per model: it is skipped while vec64 still belongs to the current model
+// (every rank bumps model_version identically, so all skip or none does).
 static scd_status shared64(scd_ctx *c) {
+  if (c->vec64_version == c->model_version) return SCD_OK;
   cudaStream_t s = c->stream;
   SCD_CK(c, cudaMemsetAsync(c->vec64, 0, sizeof(double) * (size_t)c->n_shared, s));
   k_scatter64<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->n_coord,
                                                                       c->vec64);
   SCD_CKL(c, "k_scatter64");
   ++c->launches;
-  if (c->nccl)
-    SCD_NCK(c, ncclAllReduce(c->vec64, c->vec64, (size_t)c->n_shared, ncclDouble, ncclSum, c->nccl, s));
+  if (c->has_comm()) SCD_COLL(coll_allreduce(c, c->vec64, (size_t)c->n_shared, SCD_DT_F64, SCD_OP_SUM));
+  c->vec64_version = c->model_version;
   return SCD_OK;
 }
 
@@ -141,11 +148,11 @@ scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap) {
   if (c->form == SCD_PRIMAL) {
     // rows are replicated across the feature-partitioned workers: acc[0..1] are NOT summed
     k_primal_rows<<<grid_for(c->n_shared, kT, 148 * 8), kT, 0, s>>>(c->y, c->vec64, c->n_shared, c->acc);
-    k_primal_cols<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->vec64,
-                                                                          c->n_coord, lam, N, c->acc);
+    k_primal_cols<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->y,
+                                                                          c->vec64, c->n_coord, lam, N, c->acc);
     SCD_CKL(c, "primal evaluate kernels");
     c->launches += 2;
-    if (c->nccl) SCD_NCK(c, ncclAllReduce(c->acc + 2, c->acc + 2, 3, ncclDouble, ncclSum, c->nccl, s));
+    if (c->has_comm()) SCD_COLL(coll_allreduce(c, c->acc + 2, 3, SCD_DT_F64, SCD_OP_SUM));
     SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
     SCD_CK(c, cudaStreamSynchronize(s));
     const double P = h[0] / (2.0 * N) + 0.5 * lam * h[3];
@@ -160,7 +167,7 @@ scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap) {
                                                                         c->n_coord, lam, N, c->acc);
     SCD_CKL(c, "dual evaluate kernels");
     c->launches += 2;
-    if (c->nccl) SCD_NCK(c, ncclAllReduce(c->acc + 1, c->acc + 1, 4, ncclDouble, ncclSum, c->nccl, s));
+    if (c->has_comm()) SCD_COLL(coll_allreduce(c, c->acc + 1, 4, SCD_DT_F64, SCD_OP_SUM));
     SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
     SCD_CK(c, cudaStreamSynchronize(s));
     const double P = h[1] / (2.0 * N) + h[0] / (2.0 * lam);
@@ -180,6 +187,7 @@ scd_status evaluate_group(scd_ctx *const *cs, int32_t k, double *primal, double 
   for (int i = 0; i < k; ++i) SCD_CK(cs[i], cudaStreamSynchronize(cs[i]->stream));
   cudaStream_t s = c0->stream;
   SCD_CK(c0, cudaMemsetAsync(c0->vec64, 0, sizeof(double) * (size_t)c0->n_shared, s));
+  c0->vec64_version = 0;  // now the group's sum, not ctx 0's own A x
   SCD_CK(c0, cudaMemsetAsync(c0->acc, 0, sizeof(double) * 8, s));
   for (int i = 0; i < k; ++i) {
     scd_ctx *c = cs[i];
@@ -193,8 +201,8 @@ scd_status evaluate_group(scd_ctx *const *cs, int32_t k, double *primal, double 
     k_primal_rows<<<grid_for(c0->n_shared, kT, 148 * 8), kT, 0, s>>>(c0->y, c0->vec64, c0->n_shared, c0->acc);
     for (int i = 0; i < k; ++i) {
       scd_ctx *c = cs[i];
-      k_primal_cols<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c0->vec64,
-                                                                            c->n_coord, lam, N, c0->acc);
+      k_primal_cols<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c0->y,
+                                                                            c0->vec64, c->n_coord, lam, N, c0->acc);
     }
   } else {
     k_sumsq64<<<grid_for(c0->n_shared, kT, 148 * 8), kT, 0, s>>>(c0->vec64, c0->n_shared, c0->acc + 0);

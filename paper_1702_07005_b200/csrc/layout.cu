@@ -312,6 +312,7 @@ scd_status estimate_bin_tau(scd_ctx *c, const int32_t *d_list, int64_t count, do
                             double *tau_tail) {
   cudaStream_t s = c->stream;
   double *vec = c->vec64;
+  c->vec64_version = 0;  // scratch use
   SCD_CK(c, cudaMemsetAsync(vec, 0, sizeof(double) * (size_t)c->n_shared, s));
   SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 8, s));
   const bool tail = lo >= 0 && lo < c->n_shared && tau_tail;
@@ -345,6 +346,7 @@ scd_status estimate_tail_tau(scd_ctx *c, const int32_t *d_list, int64_t count, i
                              const int32_t *idx) {
   cudaStream_t s = c->stream;
   double *vec = c->vec64;
+  c->vec64_version = 0;  // scratch use
   SCD_CK(c, cudaMemsetAsync(vec, 0, sizeof(double) * (size_t)c->n_shared, s));
   SCD_CK(c, cudaMemsetAsync(c->acc, 0, sizeof(double) * 3, s));
   // idx: the entries to count (default the matrix's; the hot-set bin passes its re-encoded copy, whose

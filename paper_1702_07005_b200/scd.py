@@ -33,11 +33,22 @@ class Matrix(C.Structure):
                 ("ptr", C.c_void_p), ("idx", C.c_void_p), ("val", C.c_void_p), ("mem", C.c_int)]
 
 
+# scd_collectives (include/scd.h): host-side transport hooks used instead of an NCCL communicator
+DT_F32, DT_F64, DT_I32, DT_I64, DT_U8 = 0, 1, 2, 3, 4
+OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class Collectives(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce", ALLREDUCE_FN), ("allgather", ALLGATHER_FN)]
+
+
 class Options(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("n_global", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_comm", C.c_void_p), ("stream", C.c_void_p), ("deterministic", C.c_int32),
                 ("max_inflight", C.c_int32), ("recompute_every", C.c_int32), ("validate", C.c_int32),
-                ("profile", C.c_int32), ("wild", C.c_int32)]
+                ("profile", C.c_int32), ("wild", C.c_int32), ("collectives", C.POINTER(Collectives))]
 
 
 class Info(C.Structure):
@@ -144,7 +155,8 @@ class Solver:
     def __init__(self, ptr, idx, val, n_rows: int, n_cols: int, y, lam: float, form: str = "dual", *,
                  seed: int = 0, deterministic: bool = False, max_inflight: int = 0, n_global: int = 0,
                  rank: int = 0, world: int = 1, nccl_comm=None, stream=None, validate: bool = True,
-                 profile: bool = False, recompute_every: int = 0, wild: bool = False):
+                 profile: bool = False, recompute_every: int = 0, wild: bool = False,
+                 collectives: Collectives | None = None):
         L = lib()
         self._form = PRIMAL if form == "primal" else DUAL
         if form not in ("primal", "dual"):
@@ -157,7 +169,7 @@ class Solver:
             raise ValueError("ptr/idx/val must all be host arrays or all CUDA tensors")
         yy, my, ky = _buf(y, np.float32)
         nnz = int(kp[-1]) if mp == MEM_HOST else int(kp[-1].item())
-        self._keep = (kp, ki, kv, ky)
+        self._keep = (kp, ki, kv, ky, collectives)
         m = Matrix(CSC if self._form == PRIMAL else CSR, n_rows, n_cols, nnz, p, i, v, mp)
         o = Options()
         L.scd_default_options(C.byref(o))
@@ -172,6 +184,8 @@ class Solver:
         o.validate = int(validate)
         o.profile = int(profile)
         o.wild = int(wild)
+        if collectives is not None:  # borrowed by the context: kept alive with it
+            o.collectives = C.pointer(collectives)
         h = C.c_void_p()
         _check(L.scd_create(C.byref(m), yy, my, float(lam), self._form, C.byref(o), C.byref(h)))
         self._h = h

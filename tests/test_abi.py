@@ -53,9 +53,10 @@ def test_binding_structs_match_the_header():
     import paper_1702_07005_b200 as p
     from paper_1702_07005_b200 import scd as b
 
-    out = (ctypes.c_int64 * 3)()
+    out = (ctypes.c_int64 * 4)()
     p.lib().scd_struct_sizes(out)
-    assert list(out) == [ctypes.sizeof(b.Matrix), ctypes.sizeof(b.Options), ctypes.sizeof(b.Info)]
+    assert list(out) == [ctypes.sizeof(b.Matrix), ctypes.sizeof(b.Options), ctypes.sizeof(b.Info),
+                         ctypes.sizeof(b.Collectives)]
 
 
 def test_status_strings():

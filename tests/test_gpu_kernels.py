@@ -140,18 +140,21 @@ def test_wild_variant_loses_updates(c3p):
     assert out[True][0] > 10 * out[False][0]
 
 
-def test_hot_set_kernel_criteo_prefix(monkeypatch):
+@pytest.mark.parametrize("implicit", [False, True], ids=["explicit_values", "implicit_values"])
+def test_hot_set_kernel_criteo_prefix(monkeypatch, implicit):
     """k_epoch_group_hot on criteo-shaped one-hot rows (BASELINE configs[4] prefix: 2 M rows x 75 M
     features, 7.8e7 entries) with λ = 0.1 so that λN = 2e5 as in each 25 M-row shard of the 8-GPU run
     (N = 200 M): the hot set is measured from the data, the window fits the staleness bound
     (grid * rows per CTA * (1 + F) <= τ), and the solution matches the oracle's optimum (BASELINE tolerances)
-    with per-epoch gaps in the sequential band."""
+    with per-epoch gaps in the sequential band.  implicit: the library gets val = NULL (NEXT-1, P:460
+    footnote: one-hot values are all 1, so they need not be stored); the oracle keeps explicit 1.0s."""
     monkeypatch.delenv("SCD_HOT", raising=False)
     cfg = synth.CONFIGS["C5"].with_rows(2_000_000)
     d = synth.gen_host(cfg)
     pr = solver.Problem.from_csr(d, lam=0.1)
     _, _, hist = solver.solve(pr, "dual", 8, seed=5)
-    s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=5)
+    assert (d["val"] == 1.0).all()
+    s = scd.Solver(d["ptr"], d["idx"], None if implicit else d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=5)
     info = s.info()
     b = info["bins"][0]
     print("schedule", info)

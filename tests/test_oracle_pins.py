@@ -204,6 +204,31 @@ def test_gap_forms_agree_and_nonnegative():
         assert ridge.primal_objective(A, pr.y, pr.lam, beta) >= ridge.dual_objective(A, pr.y, pr.lam, alpha) - 1e-12
 
 
+def test_reports_match_definitions():
+    """ridge.dual_report / primal_report (shared sparse products, used at full size) equal the
+    separate definitions at random points, and at the closed-form optimum P = D and G = 0."""
+    pr = _rand_prob(70, 30, 0.3, 32, 0.02)
+    A = pr.A()
+    rng = np.random.default_rng(3)
+    for _ in range(5):
+        beta = rng.standard_normal(pr.M) * 0.3
+        alpha = rng.standard_normal(pr.N) * 0.05
+        P, D, G = ridge.dual_report(A, pr.y, pr.lam, alpha)
+        assert P == pytest.approx(ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, alpha)),
+                                  rel=1e-12)
+        assert D == pytest.approx(ridge.dual_objective(A, pr.y, pr.lam, alpha), rel=1e-12)
+        assert G == pytest.approx(ridge.gap_dual(A, pr.y, pr.lam, alpha), rel=1e-9)
+        P, D, G = ridge.primal_report(A, pr.y, pr.lam, beta)
+        assert P == pytest.approx(ridge.primal_objective(A, pr.y, pr.lam, beta), rel=1e-12)
+        assert D == pytest.approx(ridge.dual_objective(A, pr.y, pr.lam, ridge.primal_to_dual(A, pr.y, beta)),
+                                  rel=1e-12)
+        assert G == pytest.approx(ridge.gap_primal(A, pr.y, pr.lam, beta), rel=1e-9)
+    bstar = ridge.closed_form(A, pr.y, pr.lam)
+    astar = ridge.closed_form_dual(A, pr.y, pr.lam)
+    for P, D, G in (ridge.primal_report(A, pr.y, pr.lam, bstar), ridge.dual_report(A, pr.y, pr.lam, astar)):
+        assert P == pytest.approx(D, rel=1e-12) and G <= 1e-20
+
+
 def test_gradients_finite_difference():
     """Analytic partials P:83 and P:109 vs central differences."""
     pr = _rand_prob(30, 12, 0.5, 41, 0.1)
