@@ -1,18 +1,28 @@
 #!/usr/bin/env python
 """Benchmark of the TPA-SCD hot path (Parnell et al., arXiv 1702.07005) on B200.
 
-Workload (BASELINE.json configs[2], the webspam-shaped config the metric's target is quoted on):
-C3 = 350,000 x 16,609,143 CSR, ~3,728 nnz/row (1.305e9 nnz, fp32 values + int32 indices =
-10.4 GB, larger than the 126 MB L2), dual TPA-SCD by example, λ = 1e-3.  Generated on the device
-by the seeded generator (synth/); nothing is read from disk.
+Headline workload (BASELINE.json configs[2], the webspam-shaped config the metric's target is quoted
+on): C3 = 350,000 x 16,609,143 CSR, ~3,728 nnz/row (1.306e9 nnz, fp32 values + int32 indices =
+10.4 GB, larger than the 126 MB L2), dual TPA-SCD by example, λ = 1e-3.  Generated on the device by
+the seeded generator (synth/); nothing is read from disk.
 
 A step = one local TPA-SCD epoch (scd_epoch: permutation inline, gather-dot, closed-form delta,
 atomic scatter; §8(a) rows a1-a6) and, when N > 1, one optimal-gamma aggregation round over NCCL
 (a8).  With N GPUs each rank holds its own 350,000-row block of a 350,000·N-row matrix (weak
 scaling, global N in λN).  The gap evaluation (a7) is off the clock, as in the paper's plots.
 
-Prints ONE JSON line (rank 0).  `--impl reference` times the fp64 oracle (the only "reference"
-this paper has: it ships no code) on bounded samples of the same workload on the host cores.
+Sub-records on the same JSON line:
+  N = 1: "c4_primal" (configs[3] at K = 1: C3's matrix by feature) and "c5_shard" (one GPU's
+         25 M-row shard of configs[4], implicit values), each with its epoch time, nnz/s and the
+         roofline of its dominant kernel.
+  N > 1: "north_star" — configs[4] criteo-shaped, weak-scaled at 25 M rows per rank (the full
+         200 M x 75 M at N = 8), dual by example, time and rounds to gap 1e-4 with optimal γ and with
+         the add / average baselines; and configs[3] C4 primal by feature at K = N.
+
+`python bench.py --gpus N` with N > 1 relaunches itself under torch.distributed.run (one process per
+GPU); under a launcher WORLD_SIZE must equal N.  Prints ONE JSON line (rank 0).  `--impl reference`
+times the fp64 oracle (the only "reference" this paper has: it ships no code) on bounded samples of
+the same workload on the host cores.
 """
 from __future__ import annotations
 
@@ -31,9 +41,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_NNZ = 16   # idx 4 + val 4 + shared-vector gather 4 + atomic 4
+BYTES_PER_NNZ_IMPLICIT = 12  # val = NULL (NEXT-1): no value stream
 BYTES_PER_COORD = 32  # ptr pair 16 + norm 4 + model RMW 8 + label 4
 METRIC = "nnz/s per epoch"
 METRIC_FULL = "time-to-duality-gap 1e-4 (s); nnz/s per epoch; HBM GB/s vs B200 peak"
+C5_ROWS_PER_GPU = 25_000_000
 
 
 def _env_rank():
@@ -123,6 +135,8 @@ def host_info() -> dict:
     return info
 
 
+# ------------------------------------------------------------------------------------------------
+# oracle (host) baselines: the only places bench.py executes oracle/
 def cpu_baseline(seconds: float = 15.0, rows: int = 20_000):
     """The fp64 oracle's dual epoch (Alg. 1 / Eq. 4, sequential, 1 core) on the first ``rows`` rows
     of C3; returns nnz/s over whole epochs within ~``seconds``."""
@@ -132,7 +146,7 @@ def cpu_baseline(seconds: float = 15.0, rows: int = 20_000):
 
     cfg = c3_cfg(1).with_rows(rows)
     d = synth.gen_host(cfg)
-    pr = solver.Problem.from_csr(d)
+    pr = solver.Problem.from_csr(d, csc=False)
     nrm = pr.row_norms()
     alpha, wbar = np.zeros(pr.N), np.zeros(pr.M)
     done, t0, ep = 0, time.perf_counter(), 0
@@ -147,6 +161,31 @@ def cpu_baseline(seconds: float = 15.0, rows: int = 20_000):
             "sample": f"C3 rows [0,{rows}) ({pr.nnz:.3g} nnz), {ep} sequential fp64 dual epochs (oracle.c, 1 thread)"}
 
 
+def oracle_time_to_gap(d_dev, max_epochs: int = 3, target: float = 1e-4):
+    """The sequential fp64 oracle on the FULL C3 (the same matrix, host copy): epoch time to gap 1e-4
+    (epochs on the clock, the from-scratch gap off it; SURVEY §8(d) oracle timing protocol)."""
+    import oracle
+    from oracle import ridge, solver
+
+    host = dict(ptr=d_dev["ptr"].cpu().numpy(), idx=d_dev["idx"].cpu().numpy(), val=d_dev["val"].cpu().numpy(),
+                y=d_dev["y"].cpu().numpy(), n_rows=d_dev["n_rows"], n_cols=d_dev["n_cols"], lam=d_dev["lam"])
+    pr = solver.Problem.from_csr(host, csc=False)
+    A = pr.A()
+    nrm = pr.row_norms()
+    alpha, wbar = np.zeros(pr.N), np.zeros(pr.M)
+    acc, gaps = 0.0, []
+    for t in range(1, max_epochs + 1):
+        t0 = time.perf_counter()
+        solver.dual_epoch(pr, alpha, wbar, oracle.permutation(3, t, pr.N), nrm)
+        acc += time.perf_counter() - t0
+        gaps.append(ridge.dual_report(A, pr.y, pr.lam, alpha)[2])
+        if gaps[-1] <= target:
+            break
+    return {"seconds": acc if gaps[-1] <= target else None, "epochs": len(gaps), "seconds_per_epoch": acc / len(gaps),
+            "gap_trace": [float("%.3e" % g) for g in gaps], "cores": 1,
+            "what": "full C3 (1.306e9 nnz), sequential fp64 SDCA (oracle.c), epochs to gap 1e-4"}
+
+
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
@@ -158,7 +197,7 @@ def run_reference(args):
 
     rows = 6000
     d = synth.gen_host(c3_cfg(1).with_rows(rows))
-    pr = solver.Problem.from_csr(d)
+    pr = solver.Problem.from_csr(d, csc=False)
     nrm = pr.row_norms()
     alpha, wbar = np.zeros(pr.N), np.zeros(pr.M)
     for t in range(args.warmup):
@@ -181,35 +220,137 @@ def run_reference(args):
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-ttg", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--rows", type=int, default=0, help="override rows per rank (debug only)")
-    ap.add_argument("--max-inflight", type=int, default=0)
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
-    assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_FEW_WARMUP"), "timing rules: warmup >= 3"
+# ------------------------------------------------------------------------------------------------
+class Ctx:
+    """Per-process state shared by the legs."""
 
-    import torch
+    def __init__(self, rank, world, local):
+        import torch
 
+        self.torch = torch
+        self.rank, self.world, self.local = rank, world, local
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.dist = dist
+        self.comm = None
+        self.launches = 0
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def nccl(self):
+        """The library's NCCL communicator (the library calls NCCL itself; torch only broadcasts the id)."""
+        if self.world == 1:
+            return None
+        if self.comm is None:
+            import paper_1702_07005_b200 as scd
+
+            uid = scd.nccl_unique_id() if self.rank == 0 else bytes(128)
+            t = self.torch.tensor(list(uid), dtype=self.torch.uint8, device="cuda")
+            self.dist.broadcast(t, 0)
+            self.comm = scd.nccl_comm_init(bytes(t.cpu().tolist()), self.world, self.rank)
+        return self.comm
+
+
+def kernel_roofline(s, info, kprof, bytes_per_nnz: int, el_ms: float, world: int = 1):
+    """Roofline of the dominant kernel (the bin with the most device time, CUDA events on the library
+    stream): ALGORITHMIC bytes per launch (16 B/nnz, 12 B/nnz with implicit values,
+    + 32 B/coordinate) / average launch duration vs the measured HBM copy peak."""
+    peak, peak_src = _peaks()
+    bins = info["bins"]
+    if not kprof:
+        return None
+    b_i = max(range(len(kprof)), key=lambda i: kprof[i][0])
+    ms_b, cnt_b = kprof[b_i]
+    bb = bins[b_i]
+    # one launch processes one of the n_slices slices of the bin (DESIGN.md §6)
+    bytes_launch = (bytes_per_nnz * bb["nnz"] + BYTES_PER_COORD * bb["count"]) / info["n_slices"]
+    achieved = bytes_launch / (ms_b / cnt_b / 1e3) / 1e9 if cnt_b else None
+    if bb["lanes"] >= 4096:
+        kname = "k_epoch_cluster"
+    elif bb["lanes"] >= 64:
+        kname = "k_epoch_cta_head" if bb.get("head") else "k_epoch_cta"
+    else:
+        kname = "k_epoch_group_hot" if bb.get("hot") else ("k_epoch_group_comb" if bb["lanes"] == 8 else "k_epoch_group")
+    traffic, dram_bytes = None, None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            rec = tj.get(kname) if isinstance(tj.get(kname), dict) else (tj if (kname + "<") in tj.get("kernel", "") else None)
+            if rec:
+                traffic = rec.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+           "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+           "achieved_is": f"algorithmic bytes ({bytes_per_nnz} B/nnz + 32 B/coordinate, SURVEY §8(d)) per launch / "
+                          "CUDA-event launch time",
+           "kernel": kname, "bin": b_i, "lanes": bb["lanes"], "kernel_ms_avg": ms_b / cnt_b if cnt_b else None,
+           "launches_timed": cnt_b, "kernel_share_of_step": ms_b / el_ms if el_ms else None,
+           "bytes_per_launch": bytes_launch, "peak_source": peak_src}
+    if traffic and cnt_b:
+        # measured DRAM bytes of the same kernel (ncu, per launch) over the same launch time: the shared
+        # vector's gathers and REDs mostly hit L2, so this is below the algorithmic rate (DESIGN.md §8)
+        out["dram_achieved"] = traffic / (ms_b / cnt_b / 1e3) / 1e9
+        out["dram_frac"] = out["dram_achieved"] / peak
+    return out
+
+
+def timed_epochs(ctx, s, stream, first_epoch: int, steps: int, step_fn):
+    torch = ctx.torch
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for t in range(first_epoch, first_epoch + steps):
+        step_fn(t)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    return ctx.max_over_ranks(ev0.elapsed_time(ev1))
+
+
+def time_to_gap(ctx, s, stream, step_fn, target=1e-4, max_rounds=60, first=1000):
+    """Fresh model; epoch (+ aggregation) device time accumulated until the from-scratch fp64 gap <=
+    target (reading c23: the gap is evaluated off the clock after every round)."""
+    torch = ctx.torch
+    acc, hist, g = 0.0, [], None
+    for t in range(1, max_rounds + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.barrier()
+        e0.record(stream)
+        step_fn(first + t)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        acc += ctx.max_over_ranks(e0.elapsed_time(e1))
+        g = s.duality_gap()
+        hist.append(g)
+        if g <= target or not np.isfinite(g) or g > 1e6:
+            break
+    return {"seconds": acc / 1e3 if g is not None and g <= target else None, "rounds": len(hist),
+            "gap_trace": [float("%.3e" % x) for x in hist[:40]], "target": target}
+
+
+# ------------------------------------------------------------------------------------------------
+def leg_c3(args, ctx):
+    """The headline: C3 (webspam-shaped) dual; weak-scaled C3 x N with optimal γ per epoch at N > 1."""
+    torch = ctx.torch
     import synth
     import paper_1702_07005_b200 as scd
 
-    rank, world, local = _env_rank()
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = ctx.rank, ctx.world
     cfg = c3_cfg(world)
     rows = args.rows or synth.CONFIGS["C3"].n_rows
     row0 = rank * rows
@@ -218,13 +359,7 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     nnz = int(d["ptr"][-1].item())
-    comm = None
-    if world > 1:
-        uid = scd.nccl_unique_id() if rank == 0 else bytes(128)
-        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
-        dist.broadcast(t, 0)
-        comm = scd.nccl_comm_init(bytes(t.cpu().tolist()), world, rank)
-    # The library creates its own stream; torch only wraps it to record the timing events.
+    comm = ctx.nccl()
     kw = dict(seed=3 + rank, n_global=rows * world, rank=rank, world=world, nccl_comm=comm, max_inflight=args.max_inflight)
     t_create = time.perf_counter()
     s = scd.Solver(d["ptr"], d["idx"], d["val"], rows, cfg.n_cols, d["y"], cfg.lam, "dual", profile=True, **kw)
@@ -237,64 +372,28 @@ def main():
         if world > 1:
             s.aggregate("optimal")
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
     for t in range(1, args.warmup + 1):
         step(t)
     torch.cuda.synchronize()
     s.profile_read()  # drop warm-up kernel timings
     launches0 = s.info()["launches"]
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for t in range(args.warmup + 1, args.warmup + args.steps + 1):
-            step(t)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-    el_ms = ev0.elapsed_time(ev1)
+    with ClockSampler(ctx.local) as clk:
+        el_ms = timed_epochs(ctx, s, stream, args.warmup + 1, args.steps, step)
     launches = s.info()["launches"] - launches0
     kprof = s.profile_read()
-    if dist is not None:
-        tt = torch.tensor([el_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        el_ms = float(tt.item())
     total_nnz = nnz * world
     value = total_nnz * args.steps / (el_ms / 1e3)
     ms_step = el_ms / args.steps
-
-    # roofline of the dominant kernel (the bin with the most device time)
-    peak, peak_src = _peaks()
-    bins = info["bins"]
-    b_i = max(range(len(kprof)), key=lambda i: kprof[i][0]) if kprof else 0
-    ms_b, cnt_b = kprof[b_i] if kprof else (float("nan"), 0)
-    # one launch processes one of the n_slices slices of the bin
-    bytes_launch = (BYTES_PER_NNZ * bins[b_i]["nnz"] + BYTES_PER_COORD * bins[b_i]["count"]) / info["n_slices"]
-    achieved = bytes_launch / (ms_b / cnt_b / 1e3) / 1e9 if cnt_b else None
-    bb = bins[b_i]
-    kname = ("k_epoch_split" if bb.get("split") else "k_epoch_cta_head" if bb.get("head") else "k_epoch_cta") \
-        if bb["lanes"] >= 64 else "k_epoch_group"
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            tj = json.load(open(tp))
-            # only a capture of the same kernel counts (names: "...k_epoch_cta_head<1, 256, 16>...")
-            if (kname + "<") in tj.get("kernel", ""):
-                traffic = tj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    kernel_share = (ms_b / (el_ms if world == 1 else el_ms)) if cnt_b else None
+    roof = kernel_roofline(s, info, kprof, BYTES_PER_NNZ, el_ms, world)
+    if roof and roof["kernel"] == "k_epoch_cta_head" and info.get("tail_roll"):
+        roof["kernel"] += (f" (head {info['bins'][roof['bin']]['head']} floats combined, flush every "
+                           f"{info['bins'][roof['bin']]['flush']}, head/tail gathers from the rolling read copies)")
 
     # access-pattern ceiling on this box: the same gathers + REDs over the same matrix with no
     # algorithmic dependency (tools/pattern_bench.cu), against a scratch vector
     pattern = None
     pso = os.path.join(ROOT, "tools", "libpattern.so")
-    if os.path.exists(pso):
+    if os.path.exists(pso) and not args.quick:
         import ctypes as C
 
         pl = C.CDLL(pso)
@@ -307,7 +406,6 @@ def main():
         pattern = {"ms": pms, "entries_per_s": nnz / (pms / 1e3), "epoch_over_pattern": ms_step / pms,
                    "what": "gather + red.add of sv[idx] for every stored entry, storage order, no dependencies"}
         if hasattr(pl, "pattern_run2"):
-            # the same with the gathers served from a second vector (the head kernel's tail read copy)
             pl.pattern_run2.restype = C.c_float
             pl.pattern_run2.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                         C.c_void_p]
@@ -319,30 +417,11 @@ def main():
             del scratch2
         del scratch
 
-    # time to duality gap 1e-4 from a fresh start (epoch + aggregation time only, gap off the clock)
     ttg = None
     if not args.no_ttg:
         s.set_model(np.zeros(rows, np.float32))
-        acc, hist, g = 0.0, [], None
-        for t in range(1, 61):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            barrier()
-            e0.record(stream)
-            step(1000 + t)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1)
-            if dist is not None:
-                tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                ms = float(tt.item())
-            acc += ms
-            g = s.duality_gap()
-            hist.append(g)
-            if g <= 1e-4:
-                break
-        ttg = {"seconds": acc / 1e3 if g is not None and g <= 1e-4 else None, "epochs": len(hist),
-               "gap_trace": [float("%.3e" % x) for x in hist[:12]], "target": 1e-4}
+        ttg = time_to_gap(ctx, s, stream, step)
+        ttg["epochs"] = ttg["rounds"]
     s.profile_read()
 
     # end to end through the public API with host buffers (pinned): upload + epochs (+ aggregation
@@ -358,46 +437,249 @@ def main():
             hi.copy_(d["idx"])
             hv.copy_(d["val"])
             hy.copy_(d["y"])
-            n_ep = (ttg or {}).get("epochs") or 5
+            n_ep = (ttg or {}).get("rounds") or 5
             times = []
             for rep in range(5):
                 torch.cuda.synchronize()
-                barrier()
+                ctx.barrier()
                 t0 = time.perf_counter()
-                s2 = scd.Solver(hp, hi, hv, rows, cfg.n_cols, hy, cfg.lam, "dual", validate=False, **kw)
+                # the public API's defaults, matrix validation included
+                s2 = scd.Solver(hp, hi, hv, rows, cfg.n_cols, hy, cfg.lam, "dual", **kw)
                 for t in range(1, n_ep + 1):
                     s2.epoch(t)
                     if world > 1:
                         s2.aggregate("optimal")
-                model = s2.get_model()
+                s2.get_model()
                 el = time.perf_counter() - t0
                 s2.close()
-                if dist is not None:
-                    tt = torch.tensor([el], dtype=torch.float64, device="cuda")
-                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                    el = float(tt.item())
+                el = ctx.max_over_ranks(el)
                 if rep > 0:
                     times.append(el)
             e_s = statistics.median(times)
             e2e = {"value": total_nnz * n_ep / e_s, "unit": "nnz/s",
                    "h2d_bytes_per_step": int(8 * (rows + 1) + 8 * nnz + 4 * rows),
                    "d2h_bytes_per_step": int(4 * rows), "epochs_per_step": n_ep, "seconds_per_step": e_s,
+                   "seconds_min": min(times), "seconds_median": e_s, "value_at_min": total_nnz * n_ep / min(times),
                    "seconds_per_rep": [round(x, 4) for x in times],
-                   "step": "scd_create from pinned host CSR (H2D) + epochs-to-gap-1e-4"
+                   "step": "scd_create from pinned host CSR (H2D, matrix validated) + epochs-to-gap-1e-4"
                            + (" with optimal-gamma aggregation" if world > 1 else "") + " + scd_get_model (D2H)"
                            + ("; bytes per rank" if world > 1 else "")}
             del hp, hi, hv, hy
         except Exception as ex:  # never lose the device-timed line to the e2e leg
             e2e = {"value": None, "error": f"{type(ex).__name__}: {ex}"[:300]}
+    s.close()
+    ctx.launches += launches
+    rec = {"value": value, "ms_per_step": ms_step, "nnz": nnz, "rows": rows, "cfg": cfg, "info": info, "roofline": roof,
+           "pattern": pattern, "ttg": ttg, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+           "setup_s": {"generate": t_gen, "create": t_create}}
+    return rec, d
+
+
+def leg_c4(args, ctx, d):
+    """configs[3]: C3's matrix by feature.  N = 1: K = 1 epochs (roofline of the dominant bin, time to
+    1e-4).  N > 1: columns partitioned across the ranks (partition(seed 4), c15), optimal γ rounds."""
+    torch = ctx.torch
+    import synth
+    import paper_1702_07005_b200 as scd
+
+    cfg = synth.CONFIGS["C3"]
+    N, M = cfg.n_rows, cfg.n_cols
+    if d is None or ctx.world > 1:  # N > 1: every rank needs the whole C3 (it owns columns, not rows)
+        d = synth.gen_device(cfg)
+    cp, ci, cv = scd.transpose(d["ptr"], d["idx"], d["val"], N, M, "csr")
+    y = d["y"]
+    world, rank = ctx.world, ctx.rank
+    if world > 1:
+        owner = torch.from_numpy(scd.partition(4, M, world).astype(np.int64)).cuda()
+        cols = torch.nonzero(owner == rank).flatten()
+        lens = (cp[1:] - cp[:-1])[cols]
+        sp = torch.zeros(len(cols) + 1, dtype=torch.int64, device="cuda")
+        torch.cumsum(lens, 0, out=sp[1:])
+        tot = int(sp[-1].item())
+        pos = torch.repeat_interleave(cp[cols], lens, output_size=tot) + \
+            (torch.arange(tot, device="cuda") - torch.repeat_interleave(sp[:-1], lens, output_size=tot))
+        cp, ci, cv = sp, ci[pos].contiguous(), cv[pos].contiguous()
+        del pos, owner
+        torch.cuda.empty_cache()
+    ncols = cp.numel() - 1
+    nnz = int(cp[-1].item())
+    s = scd.Solver(cp, ci, cv, N, ncols, y, cfg.lam, "primal", seed=4 + 10 * rank, profile=True, rank=rank,
+                   world=world, nccl_comm=ctx.nccl())
+    stream = torch.cuda.ExternalStream(s.stream_handle)
+    info = s.info()
+
+    def step(t):
+        s.epoch(t)
+        if world > 1:
+            s.aggregate("optimal")
+
+    for t in range(1, 4):
+        step(t)
+    torch.cuda.synchronize()
+    s.profile_read()
+    steps = 10
+    l0 = s.info()["launches"]
+    el_ms = timed_epochs(ctx, s, stream, 4, steps, step)
+    ctx.launches += s.info()["launches"] - l0
+    kprof = s.profile_read()
+    roof = kernel_roofline(s, info, kprof, BYTES_PER_NNZ, el_ms, world)
+    s.set_model(np.zeros(ncols, np.float32))
+    ttg = time_to_gap(ctx, s, stream, step, max_rounds=40 if world > 1 else 10)
+    s.close()
+    del cp, ci, cv
+    torch.cuda.empty_cache()
+    return {"workload": "C4 (BASELINE configs[3]): C3's matrix by feature, primal TPA-SCD (CSC)"
+                        + (f", columns partitioned across {world} GPUs, optimal-gamma aggregation over NCCL each round"
+                           if world > 1 else ", K = 1"),
+            "nnz_per_gpu": nnz, "columns_per_gpu": ncols, "ms_per_step": el_ms / steps,
+            "nnz_per_s": nnz * world * steps / (el_ms / 1e3), "steps": steps, "roofline": roof,
+            "time_to_gap": ttg, "schedule": [{k: b[k] for k in ("lanes", "count", "nnz", "grid", "cap", "snap")}
+                                             for b in info["bins"]]}
+
+
+def leg_c5(args, ctx):
+    """configs[4]: criteo-shaped 200 M x 75 M one-hot, values implicit (val = NULL, NEXT-1), dual by
+    example, 25 M rows per GPU (global N = 25 M x N: 200 M at N = 8).  N = 1: one shard's epoch (the
+    per-GPU compute of the 8-GPU run, λN of the 8-GPU run).  N > 1: rounds of epoch + aggregation to
+    gap 1e-4 with optimal γ, and the add / average baselines."""
+    torch = ctx.torch
+    import synth
+    import paper_1702_07005_b200 as scd
+
+    world, rank = ctx.world, ctx.rank
+    rows = C5_ROWS_PER_GPU
+    cfg = synth.CONFIGS["C5"].with_rows(rows * max(world, 8 if world == 1 else world))
+    n_global = rows * 8 if world == 1 else rows * world
+    d = synth.gen_device(cfg, rank * rows, rows)
+    assert bool((d["val"] == 1.0).all())
+    d["val"] = None
+    torch.cuda.empty_cache()
+    nnz = int(d["ptr"][-1].item())
+    comm = ctx.nccl()
+    out = {"workload": f"C5 criteo-shaped (BASELINE configs[4]): {rows} rows x {cfg.n_cols} features per GPU, "
+                       f"39 one-hot fields, implicit values (val = NULL), dual by example, global N = {n_global}",
+           "nnz_per_gpu": nnz, "rows_per_gpu": rows, "n_global": n_global}
+    if world == 1:
+        s = scd.Solver(d["ptr"], d["idx"], None, rows, cfg.n_cols, d["y"], cfg.lam, "dual", seed=5, n_global=n_global,
+                       profile=True)
+        stream = torch.cuda.ExternalStream(s.stream_handle)
+        info = s.info()
+        for t in range(1, 4):
+            s.epoch(t)
+        torch.cuda.synchronize()
+        s.profile_read()
+        steps = 10
+        l0 = s.info()["launches"]
+        el_ms = timed_epochs(ctx, s, stream, 4, steps, s.epoch)
+        ctx.launches += s.info()["launches"] - l0
+        kprof = s.profile_read()
+        out.update({"ms_per_step": el_ms / steps, "nnz_per_s": nnz * steps / (el_ms / 1e3), "steps": steps,
+                    "roofline": kernel_roofline(s, info, kprof, BYTES_PER_NNZ_IMPLICIT, el_ms),
+                    "schedule": [{k: b[k] for k in ("lanes", "count", "nnz", "grid", "block", "flush", "hot", "tau")}
+                                 for b in info["bins"]],
+                    "note": "one GPU's shard of the 8-GPU run (epoch only; the round adds the 300 MB all-reduce)"})
+        s.close()
+        return out
+    s = scd.Solver(d["ptr"], d["idx"], None, rows, cfg.n_cols, d["y"], cfg.lam, "dual", seed=5 + rank,
+                   n_global=n_global, rank=rank, world=world, nccl_comm=comm)
+    stream = torch.cuda.ExternalStream(s.stream_handle)
+    modes = {}
+    for mode, max_rounds in (("optimal", 30), ("average", 15), ("add", 4)):
+        s.set_model(np.zeros(rows, np.float32))
+        ttg = time_to_gap(ctx, s, stream, lambda t: (s.epoch(t), s.aggregate(mode)), max_rounds=max_rounds,
+                          first=2000 * (1 + len(modes)))
+        modes[mode] = ttg
+    s.close()
+    out["modes"] = modes
+    out["time_to_gap_1e-4_s"] = modes["optimal"]["seconds"]
+    out["rounds_to_gap_1e-4"] = modes["optimal"]["rounds"] if modes["optimal"]["seconds"] else None
+    return out
+
+
+# ------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ttg", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the C4 / C5 sub-records")
+    ap.add_argument("--quick", action="store_true", help="skip the access-pattern ceiling and the oracle time-to-gap")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--rows", type=int, default=0, help="override rows per rank (debug only)")
+    ap.add_argument("--max-inflight", type=int, default=0)
+    args = ap.parse_args()
+    rank, world, local = _env_rank()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: relaunch under torch.distributed.run (the driver's own launch sets WORLD_SIZE)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={29400 + os.getpid() % 500}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: one process per GPU is required"}),
+              flush=True)
+        return 2
+    if args.impl == "reference":
+        return run_reference(args)
+    assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_FEW_WARMUP"), "timing rules: warmup >= 3"
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the driver can check the rank count / transport in the log
+    ctx = Ctx(rank, world, local)
+    rec, d = leg_c3(args, ctx)
+    subs = {}
+    if not args.no_sub:
+        # sub-records / north-star legs (DESIGN.md §8); a failing leg never loses the headline line
+        if world == 1:
+            try:
+                subs["c4_primal"] = leg_c4(args, ctx, d)
+            except Exception as ex:
+                subs["c4_primal"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+            oracle_ttg = None
+            if rank == 0 and not args.quick and not args.no_cpu_baseline:
+                try:
+                    oracle_ttg = oracle_time_to_gap(d)
+                except Exception as ex:
+                    oracle_ttg = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+            del d
+            torch.cuda.empty_cache()
+            try:
+                subs["c5_shard"] = leg_c5(args, ctx)
+            except Exception as ex:
+                subs["c5_shard"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+        else:
+            oracle_ttg = None
+            del d
+            torch.cuda.empty_cache()
+            ns = {}
+            for name, fn in (("c5_criteo", lambda: leg_c5(args, ctx)), ("c4_by_feature", lambda: leg_c4(args, ctx, None))):
+                try:
+                    ns[name] = fn()
+                except Exception as ex:
+                    ns[name] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+                torch.cuda.empty_cache()
+            subs["north_star"] = ns
+    else:
+        oracle_ttg = None
+        del d
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_seconds)
+        if oracle_ttg:
+            cpu["time_to_gap_1e-4"] = oracle_ttg
 
     if rank == 0:
+        cfg, info, rows, nnz, ttg = rec["cfg"], rec["info"], rec["rows"], rec["nnz"], rec["ttg"]
         out = {
-            "metric": METRIC, "metric_full": METRIC_FULL, "value": value, "unit": "nnz/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "metric": METRIC, "metric_full": METRIC_FULL, "value": rec["value"], "unit": "nnz/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C3 webspam-shaped (BASELINE configs[2]): dual TPA-SCD by example, "
                                    f"{rows}x{cfg.n_cols} per GPU, {nnz} nnz/GPU, lambda=1e-3"
@@ -405,33 +687,26 @@ def main():
                        "form": "dual", "rows_per_gpu": rows, "n_cols": cfg.n_cols, "nnz_per_gpu": nnz,
                        "lambda": cfg.lam, "l2": "inputs larger than L2 (10.4 GB CSR per GPU, 126 MB L2)",
                        "parallelism": f"dp{world}" if world > 1 else "single GPU",
-                       "schedule": bins, "inflight_cap": info["inflight_cap"], "tau_star": info["tau_star"],
+                       "schedule": info["bins"], "inflight_cap": info["inflight_cap"], "tau_star": info["tau_star"],
                        "tail_read_copy": bool(info.get("tail_snap")), "tail_tau": info.get("tail_tau"),
-                       "tail_roll": info.get("tail_roll"), "n_slices": info.get("n_slices")},
+                       "tail_roll": info.get("tail_roll"), "head_copy": info.get("head_copy"),
+                       "n_slices": info.get("n_slices")},
             "time_to_gap_1e-4_s": (ttg or {}).get("seconds"), "time_to_gap": ttg,
-            "hbm_gbs": (BYTES_PER_NNZ * total_nnz + BYTES_PER_COORD * rows * world) / (ms_step / 1e3) / 1e9,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": f"{kname} (bin {b_i}, {bb['lanes']} lanes/coord"
-                                   + (f", head {bb['head']} floats combined, flush every {bb['flush']}" if bb.get("head") else "")
-                                   + ((", tail gathers from the read copy refreshed in rolling chunks (one launch per epoch)"
-                                       if info.get("tail_roll") else ", tail gathers from the per-slice read copy")
-                                      if bb.get("head") and info.get("tail_snap") else "")
-                                   + ")",
-                         "kernel_ms_avg": ms_b / cnt_b if cnt_b else None, "kernel_share_of_step": kernel_share,
-                         "bytes_per_launch": bytes_launch, "peak_source": peak_src,
-                         "byte_model": "16 B/nnz (idx+val+gather+atomic) + 32 B/coordinate"},
-            "access_pattern_ceiling": pattern,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "setup_s": {"generate": t_gen, "create": t_create},
+            "hbm_gbs": (BYTES_PER_NNZ * nnz * world + BYTES_PER_COORD * rows * world) / (rec["ms_per_step"] / 1e3) / 1e9,
+            "roofline": rec["roofline"],
+            "access_pattern_ceiling": rec["pattern"],
+            "cpu_baseline": cpu, "e2e": rec["e2e"], "gpu_launches": rec["gpu_launches"],
+            "gpu_launches_all_legs": ctx.launches,
+            "clocks": rec["clocks"], "setup_s": rec["setup_s"],
+            **subs,
         }
-        print(json.dumps(out), flush=True)
-    s.close()
-    if comm:
-        scd.nccl_comm_destroy(comm)
-    if dist is not None:
-        dist.destroy_process_group()
+        print(json.dumps(out, default=float), flush=True)
+    if ctx.comm:
+        import paper_1702_07005_b200 as scd
+
+        scd.nccl_comm_destroy(ctx.comm)
+    if ctx.dist is not None:
+        ctx.dist.destroy_process_group()
     return 0
 
 

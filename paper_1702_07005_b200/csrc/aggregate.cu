@@ -307,7 +307,15 @@ scd_status aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
     SCD_COLL(coll_allreduce(c, c->acc, 6, SCD_DT_F64, SCD_OP_SUM));  // acc[3..4] are still 0 here
     SCD_COLL(coll_group_end(c));
   }
-  k_shared_dots<<<grid_for(ns, kT), kT, 0, s>>>(c->sv0, c->comm, ns, c->acc);
+  {
+    // <sv0, Δ> and ||Δ||² over the replicated vectors: each rank sums its 1/K shard and the partial
+    // sums are all-reduced, so every rank derives the bit-identical γ (a rank-local sum of the whole
+    // vector rounds differently from rank to rank: fp64 atomics in block_sum_atomic)
+    const int K = c->has_comm() ? c->opt.world : 1, r = c->has_comm() ? c->opt.rank : 0;
+    const int64_t lo = ns * r / K, hi = ns * (r + 1) / K;
+    k_shared_dots<<<grid_for(std::max<int64_t>(hi - lo, 1), kT), kT, 0, s>>>(c->sv0 + lo, c->comm + lo, hi - lo, c->acc);
+    if (c->has_comm() && K > 1) SCD_COLL(coll_allreduce(c, c->acc + 3, 2, SCD_DT_F64, SCD_OP_SUM));
+  }
   k_gamma<<<1, 1, 0, s>>>(c->acc, (int)mode, (int)c->form, (double)c->opt.world, c->lam, (double)c->n_global);
   k_apply_shared<<<grid_for(ns, kT), kT, 0, s>>>(c->sv, c->sv0, c->comm, ns, c->acc);
   k_apply_model<<<grid_for(nc, kT), kT, 0, s>>>(c->x, c->x0, nc, c->acc);

@@ -172,6 +172,7 @@ struct scd_ctx {
   bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)
   int64_t head_copy = 0;              // experiment: head gathers from svr[0, H) refreshed every head_copy rows per chunk
   bool head_pf = true;                // head kernel prefetches the next coordinate (SCD_HEAD_PF=0: off)
+  int head_T = 256;                   // threads per CTA of the head kernel (SCD_HEAD_T=512: experiment)
   int tail_snap = 0;                  // head kernel reads the tail [tail_lo, tail_hi) of the shared vector from a
                                       // read copy refreshed before every slice: 1 = L2 loads, 2 = L1-cached loads
   float *svr = nullptr;               // device [n_shared]: the read copy (only [tail_lo, tail_hi) is maintained)

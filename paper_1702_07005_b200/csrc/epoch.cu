@@ -356,7 +356,7 @@ __device__ __forceinline__ float ld_tail(const EpochArgs &a, int32_t j) {
 // path.  The prefetched coordinate reads nothing of the shared vector before its turn, so this adds
 // no staleness; x[c'] is current because this CTA is its only writer in the epoch (c10).
 template <int FORM, int T, int E, bool SNAP, int TS = 0, bool PF = false, bool HC = false>
-__global__ void __launch_bounds__(T, 4) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
+__global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
   constexpr int NW = T / 32;
   extern __shared__ float4 s_dyn[];
   float *s_acc = reinterpret_cast<float *>(s_dyn);
@@ -1380,7 +1380,8 @@ void *bin_kernel(const scd_ctx *c, const Bin &b) {
                              : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true, 1>;
   if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && !c->head_snap && c->form == SCD_DUAL) {
     if (c->head_pf && c->head_copy > 0 && c->tail_snap == 1)
-      return (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true, true>;
+      return c->head_T == 512 ? (void *)k_epoch_cta_head<SCD_DUAL, 512, kCtaE, false, 1, true, true>
+                              : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true, true>;
     if (c->head_pf)
       return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 2, true>
                                : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true>;
@@ -1540,7 +1541,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
   const bool comb = (b.lanes == 8 && !b.plain && group_kind() == 2);  // fixed CTA size (kernel template)
-  int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : kCtaT));
+  int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : (b.head > 0 ? c->head_T : kCtaT)));
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
   if (group && !comb && b.cap > 0 && b.cap * b.lanes < block) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);

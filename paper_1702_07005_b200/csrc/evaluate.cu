@@ -9,6 +9,8 @@
 //   P(β̂)   with β̂ = v/λ (Eq. 5): ||q/λ - y||²/(2N) + ||v||²/(2λ)
 //   D(α)   = -N/2||α||² - ||v||²/(2λ) + αᵀy
 //   G_D    = ||y - Nα - q/λ||²/(2N) = ||∇D(α)||²/(2N)                   (c13)
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace scd {
@@ -146,13 +148,17 @@ scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap) {
   const double N = (double)c->n_global, lam = c->lam;
   double h[8] = {0};
   if (c->form == SCD_PRIMAL) {
-    // rows are replicated across the feature-partitioned workers: acc[0..1] are NOT summed
-    k_primal_rows<<<grid_for(c->n_shared, kT, 148 * 8), kT, 0, s>>>(c->y, c->vec64, c->n_shared, c->acc);
+    // rows are replicated across the feature-partitioned workers: each rank sums its 1/K shard of them
+    // and everything is all-reduced once (every rank then holds bit-identical results)
+    const int K = c->has_comm() ? c->opt.world : 1, r = c->has_comm() ? c->opt.rank : 0;
+    const int64_t lo = c->n_shared * r / K, hi = c->n_shared * (r + 1) / K;
+    k_primal_rows<<<grid_for(std::max<int64_t>(hi - lo, 1), kT, 148 * 8), kT, 0, s>>>(c->y + lo, c->vec64 + lo, hi - lo,
+                                                                                    c->acc);
     k_primal_cols<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->y,
                                                                           c->vec64, c->n_coord, lam, N, c->acc);
     SCD_CKL(c, "primal evaluate kernels");
     c->launches += 2;
-    if (c->has_comm()) SCD_COLL(coll_allreduce(c, c->acc + 2, 3, SCD_DT_F64, SCD_OP_SUM));
+    if (c->has_comm()) SCD_COLL(coll_allreduce(c, c->acc, 5, SCD_DT_F64, SCD_OP_SUM));
     SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
     SCD_CK(c, cudaStreamSynchronize(s));
     const double P = h[0] / (2.0 * N) + 0.5 * lam * h[3];
@@ -161,13 +167,15 @@ scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap) {
     if (dual) *dual = D;
     if (gap) *gap = h[2] / (2.0 * lam);
   } else {
-    // v is replicated across the example-partitioned workers: acc[0] is NOT summed
-    k_sumsq64<<<grid_for(c->n_shared, kT, 148 * 8), kT, 0, s>>>(c->vec64, c->n_shared, c->acc + 0);
+    // v is replicated across the example-partitioned workers: each rank sums ||v||² over its 1/K shard
+    const int K = c->has_comm() ? c->opt.world : 1, r = c->has_comm() ? c->opt.rank : 0;
+    const int64_t lo = c->n_shared * r / K, hi = c->n_shared * (r + 1) / K;
+    k_sumsq64<<<grid_for(std::max<int64_t>(hi - lo, 1), kT, 148 * 8), kT, 0, s>>>(c->vec64 + lo, hi - lo, c->acc + 0);
     k_dual_rows<<<grid_for(c->n_coord * 32, kT, 148 * 32), kT, 0, s>>>(c->ptr, c->idx, c->val, c->x, c->y, c->vec64,
                                                                         c->n_coord, lam, N, c->acc);
     SCD_CKL(c, "dual evaluate kernels");
     c->launches += 2;
-    if (c->has_comm()) SCD_COLL(coll_allreduce(c, c->acc + 1, 4, SCD_DT_F64, SCD_OP_SUM));
+    if (c->has_comm()) SCD_COLL(coll_allreduce(c, c->acc, 5, SCD_DT_F64, SCD_OP_SUM));
     SCD_CK(c, cudaMemcpyAsync(h, c->acc, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
     SCD_CK(c, cudaStreamSynchronize(s));
     const double P = h[1] / (2.0 * N) + h[0] / (2.0 * lam);

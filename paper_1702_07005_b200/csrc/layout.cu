@@ -429,6 +429,7 @@ scd_status build_schedule(scd_ctx *c) {
   }
   if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
   c->head_pf = !(getenv("SCD_HEAD_PF") && atoi(getenv("SCD_HEAD_PF")) == 0);
+  c->head_T = getenv("SCD_HEAD_T") && atoi(getenv("SCD_HEAD_T")) == 512 ? 512 : 256;
   c->head_copy = 0;
   // one binning pass with the medium-row boundary lim1 (launch order: longest coordinates first)
   auto bin_pass = [&](int64_t l1) -> scd_status {
@@ -515,7 +516,7 @@ scd_status build_schedule(scd_ctx *c) {
       // either refreshed between slices (a slice within the bound) or, with one head bin, in rolling
       // chunks whose full sweep is within the bound (possible with a shorter sweep than a slice)
       const bool roll_env_off = getenv("SCD_TAIL_ROLL") && atoi(getenv("SCD_TAIL_ROLL")) == 0;
-      const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
+      const int64_t nch = (c->tail_hi - c->tail_lo + 4 * c->head_T - 1) / (4 * c->head_T);
       const bool can_roll = c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf &&
                             !c->head_snap && nch > 0 &&
                             std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0) >= (double)nch;
@@ -535,7 +536,7 @@ scd_status build_schedule(scd_ctx *c) {
       if (c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf && !c->head_snap &&
           c->opt.max_inflight == 0) {
         const Bin &B = c->bins[bi];
-        const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
+        const int64_t nch = (c->tail_hi - c->tail_lo + 4 * c->head_T - 1) / (4 * c->head_T);
         const double sweep = std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0);
         const int64_t R = nch > 0 ? (int64_t)(sweep / (double)nch) : 0;
         if (R >= 1) {
@@ -552,7 +553,7 @@ scd_status build_schedule(scd_ctx *c) {
       Bin &HB = c->bins[bi];
       const char *hce = getenv("SCD_HEAD_COPY");
       if (c->tail_roll > 0 && HB.head > 0 && !(hce && atoll(hce) == 0)) {
-        const int64_t nchh = (HB.head + 4 * kLanesCta - 1) / (4 * kLanesCta);
+        const int64_t nchh = (HB.head + 4 * c->head_T - 1) / (4 * c->head_T);
         const double budget = combine_budget(c, HB);
         int64_t P = 0;
         int f = HB.flush;
