@@ -213,11 +213,6 @@ typedef struct {
   int32_t bin_head[4];    /* per bin: > 0 = the CTA kernel combines updates of sv[0, bin_head) in shared
                              memory (head-combining kernel); 0 = plain */
   int32_t bin_flush[4];   /* per bin: coordinates per CTA between flushes of the combined head */
-  int32_t bin_split[4];   /* per bin: 1 = die-split kernel (each coordinate split over the two dies) */
-  int32_t die_split;      /* 1 = the two-die placement is active */
-  int32_t n_die_sm[2];    /* SMs found on each die by the create-time probe */
-  float die_lat[2];       /* probe: near / far atomic round-trip latency (SM cycles) */
-  int64_t split_nnz0;     /* die split: stored entries whose shared-vector element is homed on die 0 */
   int32_t bin_hot[4];     /* per bin: > 0 = hot-set kernel with this many hot shared-vector entries (hot.cu) */
   double hot_cover;       /* share of the hot bin's stored entries that fall on a hot entry */
   int32_t tail_snap;      /* head kernel: 1 = tail gathers (ids >= bin_head) read a copy of the shared vector

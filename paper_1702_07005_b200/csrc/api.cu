@@ -55,16 +55,9 @@ void free_ctx(scd_ctx *c) {
   cudaFree(c->empty_list);
   for (int i = 0; i < kMaxBins; ++i) cudaFree(c->bins[i].list);
   cudaFree(c->counters);
-  cudaFree(c->sm_die);
   cudaFree(c->hot_idx);
   cudaFree(c->hot_ids);
   cudaFree(c->hot_hc);
-  cudaFree(c->split_mid);
-  cudaFree(c->split_idx);
-  cudaFree(c->split_val);
-  cudaFree(c->slot_p);
-  cudaFree(c->slot_tag);
-  cudaFree(c->split_err);
   cudaFree(c->acc);
   cudaFree(c->vec64);
   cudaFree(c->comm);
@@ -332,8 +325,6 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
       if ((st = tune_shared_layout(c)) != SCD_OK) return bail(st);
     }
   }
-  // two-die placement of the CTA bins (die.cu); uses the final shared-vector placement
-  if ((st = setup_die_split(c)) != SCD_OK) return bail(st);
   // initial state (Alg. 1/2 "Initialize: β = 0, w = 0"): model 0; primal residual r = y - 0 = y; w̄ = 0
   if (form == SCD_PRIMAL) {
     cudaMemcpyAsync(c->sv, c->y, sizeof(float) * (size_t)c->n_shared, cudaMemcpyDeviceToDevice, s);
@@ -377,14 +368,12 @@ scd_status scd_epoch(scd_ctx *c, uint32_t epoch) {
 
 scd_status scd_objective(scd_ctx *c, double *primal, double *dual) {
   CK_CTX(c);
-  if (scd_status st = check_split_error(c); st != SCD_OK) return st;
   return evaluate(c, primal, dual, nullptr);
 }
 
 scd_status scd_duality_gap(scd_ctx *c, double *gap) {
   CK_CTX(c);
   if (!gap) return fail(c, SCD_E_INVALID_ARG, "gap is NULL");
-  if (scd_status st = check_split_error(c); st != SCD_OK) return st;
   return evaluate(c, nullptr, nullptr, gap);
 }
 
@@ -393,7 +382,6 @@ scd_status scd_aggregate(scd_ctx *c, scd_agg mode, double *gamma) {
   if (mode != SCD_AGG_ADD && mode != SCD_AGG_AVERAGE && mode != SCD_AGG_OPTIMAL)
     return fail(c, SCD_E_INVALID_ARG, "bad aggregation mode");
   if (c->opt.world > 1 && !c->has_comm()) return fail(c, SCD_E_STATE, "no communicator");
-  if (scd_status st = check_split_error(c); st != SCD_OK) return st;
   scd_status st = aggregate(c, mode, gamma);
   if (st != SCD_OK) return st;
   ++c->model_version;
@@ -445,7 +433,7 @@ scd_status scd_get_model(scd_ctx *c, float *host_out, int64_t len) {
   if (!host_out || len != c->n_coord) return fail(c, SCD_E_INVALID_ARG, "model length mismatch");
   SCD_CK(c, cudaMemcpyAsync(host_out, c->x, sizeof(float) * (size_t)len, cudaMemcpyDeviceToHost, c->stream));
   SCD_CK(c, cudaStreamSynchronize(c->stream));
-  return check_split_error(c);
+  return SCD_OK;
 }
 
 scd_status scd_get_shared(scd_ctx *c, float *host_out, int64_t len) {
@@ -511,12 +499,6 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
     if (i == 0 || c->probe_ms[i] < info->probe_best_ms) info->probe_best_ms = c->probe_ms[i];
     if (c->probe_ms[i] > info->probe_worst_ms) info->probe_worst_ms = c->probe_ms[i];
   }
-  info->die_split = c->die_split ? 1 : 0;
-  info->n_die_sm[0] = c->n_die_sm[0];
-  info->n_die_sm[1] = c->n_die_sm[1];
-  info->die_lat[0] = c->die_lat[0];
-  info->die_lat[1] = c->die_lat[1];
-  info->split_nnz0 = c->split_nnz0;
   info->hot_cover = c->hot_cover;
   info->tail_snap = c->tail_snap;
   info->tail_tau = c->tail_tau;
@@ -532,7 +514,6 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
     info->bin_tau[i] = c->bins[i].tau;
     info->bin_head[i] = c->bins[i].head;
     info->bin_flush[i] = c->bins[i].flush;
-    info->bin_split[i] = c->bins[i].split;
     info->bin_hot[i] = c->bins[i].hot;
     info->bin_snap[i] = c->bins[i].snap;
     if (c->bins[i].cap > info->inflight_cap) info->inflight_cap = c->bins[i].cap;

@@ -13,8 +13,6 @@
 namespace scd {
 
 constexpr int kMaxBins = 4;
-constexpr int kMaxSm = 256;           // SM ids (die map size)
-constexpr int kDieChunkFloats = 512;  // 2 KB: granularity of the address -> die (L2 home) map
 constexpr int kMaxSlices = 64;
 // shared-vector placement candidates (bytes into its allocation), epoch.cu tune_shared_layout
 constexpr int kSvCandidates = 18;
@@ -91,7 +89,6 @@ struct Bin {
   int plain = 0;             // 1 = plain sub-warp kernel (cap below the combining kernel's CTA batch)
   int head = 0;              // CTA bins: > 0 = head-combining kernel over sv[0, head) (k_epoch_cta_head)
   int flush = 0;             // head kernel: coordinates per CTA between flushes of the pending head
-  int split = 0;             // CTA bins: 1 = die-split kernel (k_epoch_split, die.cu)
   int cl = kClusterCtas;     // cluster bin: CTAs per cluster (one coordinate per cluster)
   int hot = 0;               // 8-lane bin: > 0 = hot-set kernel with this many hot slots (hot.cu)
   int snap = 0;              // 1 = every slice launch gathers from a copy of the shared vector taken just
@@ -158,8 +155,6 @@ struct scd_ctx {
   int64_t launches = 0;
   uint32_t epochs_done = 0;
   double tau_star = 0.0;   // smallest estimated staleness bound over the bins (layout.cu)
-  // die-split epoch (die.cu): SM -> die map, each coordinate's entries reordered so
-  // the ones whose shared-vector entry is homed in die 0's L2 come first
   int32_t *hot_idx = nullptr;         // device [nnz]: re-encoded indices for the hot-set kernel (hot.cu)
   int32_t *hot_ids = nullptr;         // device [K]: shared-vector index of each hot slot
   bool hot_hp = false;                // hot-set kernel also gathers the next batch's hot values (from the copy) early
@@ -167,14 +162,10 @@ struct scd_ctx {
   double hot_tail_tau = 0.0;          // staleness bound of the hot bin's coupling through its non-hot entries
   int64_t hot_copy = 0;               // hot-set kernel: > 0 = hot values gathered from the rolling copy hot_hc (period)
   float *hot_hc = nullptr;            // device [K]: rolling copy of the hot values in slot order
-  bool hot_view = false;              // hot-set kernel also keeps a per-CTA view of the hot values
   double hot_cover = 0.0;             // share of the bin's entries that are hot
-  bool head_snap = false;             // head kernel also serves head gathers from a per-CTA view (SCD_HEAD_SNAP=1)
-  int64_t head_copy = 0;              // experiment: head gathers from svr[0, H) refreshed every head_copy rows per chunk
-  bool head_pf = true;                // head kernel prefetches the next coordinate (SCD_HEAD_PF=0: off)
-  int head_T = 256;                   // threads per CTA of the head kernel (SCD_HEAD_T=512: experiment)
-  int tail_snap = 0;                  // head kernel reads the tail [tail_lo, tail_hi) of the shared vector from a
-                                      // read copy refreshed before every slice: 1 = L2 loads, 2 = L1-cached loads
+  int64_t head_copy = 0;              // > 0: head gathers from svr[0, H), one chunk refreshed every head_copy rows
+  int tail_snap = 0;                  // 1: the head kernel reads the tail [tail_lo, tail_hi) of the shared vector
+                                      // from the read copy svr (rolling refresh, or before every slice)
   float *svr = nullptr;               // device [n_shared]: the read copy (only [tail_lo, tail_hi) is maintained)
   int64_t tail_lo = 0, tail_hi = 0;
   int64_t sv_active = 0;              // dual: w̄ is zero beyond [0, sv_active) on every rank (aggregation extent)
@@ -182,20 +173,6 @@ struct scd_ctx {
   double tail_tau = 0.0;              // staleness bound of the head bin's coupling through the tail entries
   int64_t tail_roll = 0;              // > 0: the tail copy is refreshed chunk by chunk inside the epoch (every
                                       // tail_roll-th row one 1024-float chunk) instead of between slices
-  bool die_split = false;
-  uint8_t *sm_die = nullptr;          // device [kMaxSm]: die of each SM id
-  int n_die_sm[2] = {0, 0};
-  int64_t *split_mid = nullptr;       // device [n_coord]: first die-1 entry of coordinate c
-  int32_t *split_idx = nullptr;       // device [nnz]: entries reordered per coordinate (die 0, die 1)
-  float *split_val = nullptr;         // device [nnz] (nullptr for implicit values)
-  float *slot_p = nullptr;            // device [2 * max bin count]: partial dot per (position, die)
-  unsigned *slot_tag = nullptr;       // device [2 * max bin count]: launch tag of the partial
-  unsigned *split_err = nullptr;      // device: rendezvous timeout flag
-  unsigned launch_tag = 0;
-  int64_t split_nnz0 = 0;             // stored entries homed on die 0 (whole matrix)
-  bool split_nosync = false;          // diagnostic (SCD_SPLIT_NOSYNC=1): skip the partner exchange — WRONG results,
-                                      // measures the cost of the rendezvous only
-  float die_lat[2] = {0, 0};          // probe: median near / far atomic latency (cycles)
   std::string err;
 };
 
@@ -263,9 +240,6 @@ scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int3
 // hot.cu ---------------------------------------------------------------------------------------
 scd_status setup_hot(scd_ctx *c);
 
-// die.cu ---------------------------------------------------------------------------------------
-scd_status setup_die_split(scd_ctx *c);
-scd_status check_split_error(scd_ctx *c);
 
 // evaluate.cu ----------------------------------------------------------------------------------
 scd_status evaluate(scd_ctx *c, double *primal, double *dual, double *gap);

@@ -135,110 +135,8 @@ __device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
 }
 
 // ----------------------------------------------------------------------------------------------
-// Two-pass streaming CTA kernel (one coordinate per CTA).  Pass 1 streams the coordinate's
-// (idx, val) from HBM with coalesced loads, U independent gathers in flight per thread; pass 2
-// re-reads (idx, val) — now L2-resident — for the atomic scatter.  Holding nothing in registers
-// between the passes keeps the kernel at ~32 registers, i.e. full occupancy (64 warps/SM), which
-// is what hides the idx -> gather -> reduce -> scatter latency chain (the register-resident
-// variant below ran at 50% occupancy and was latency-bound).  Thread 0 software-pipelines the
-// schedule: the next ticket's atomic is issued before pass 1 and its coordinate / offsets are
-// fetched before pass 2, so neither latency sits on the critical path.
-template <int FORM, int T, int U, int MINB>
-__global__ void __launch_bounds__(T, MINB) k_epoch_stream(EpochArgs a, BinArgs b) {
-  constexpr int NW = T / 32;
-  __shared__ float s_red[NW];
-  __shared__ float s_delta;
-  __shared__ long long s_c, s_beg, s_end;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // thread 0: schedule state for the next coordinate
-  long long nc = -1, nbeg = 0, nend = 0;
-  if (tid == 0) {
-    const int64_t t = b.lo + (int64_t)atomicAdd(b.counter, 1u);
-    if (t < b.hi) {
-      nc = bin_coord(b, (uint64_t)t);
-      nbeg = __ldg(a.ptr + nc);
-      nend = __ldg(a.ptr + nc + 1);
-    }
-  }
-  for (;;) {
-    unsigned int nticket = 0;
-    if (tid == 0) {
-      s_c = nc;
-      s_beg = nbeg;
-      s_end = nend;
-      if (nc >= 0) nticket = atomicAdd(b.counter, 1u);  // next ticket, consumed after pass 1
-    }
-    __syncthreads();
-    const long long c = s_c;
-    if (c < 0) break;
-    const int64_t beg = s_beg, end = s_end;
-    float xc = 0.f, nrm = 0.f, yc = 0.f;
-    if (tid == 0) {  // consumed after the reduction
-      xc = a.x[c];
-      nrm = __ldg(a.norm + c);
-      if (FORM == SCD_DUAL) yc = __ldg(a.y + c);
-    }
-    // pass 1: gather-dot
-    float acc = 0.f;
-    for (int64_t base = beg + tid; base < end; base += (int64_t)T * U) {
-      int32_t id[U];
-      float v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t k = base + (int64_t)u * T;
-        id[u] = k < end ? __ldcg(a.idx + k) : -1;
-        v[u] = k < end ? val_cg(a.val, k) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (id[u] >= 0) acc = fmaf(ld_sv(a.svg + id[u]), v[u], acc);
-    }
-    if (tid == 0) {  // schedule the next coordinate while the block reduces / scatters
-      const int64_t t = b.lo + (int64_t)nticket;
-      nc = -1;
-      if (t < b.hi) {
-        nc = bin_coord(b, (uint64_t)t);
-        nbeg = __ldg(a.ptr + nc);
-        nend = __ldg(a.ptr + nc + 1);
-      }
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) s_red[wid] = acc;
-    __syncthreads();
-    if (wid == 0) {
-      float s = lane < NW ? s_red[lane] : 0.f;
-      s = warp_sum(s);
-      if (lane == 0) {
-        const float d = coord_delta<FORM>(s, xc, nrm, yc, a.lam, a.lamN);
-        if (!b.dry) a.x[c] = xc + d;  // single writer per epoch (c10)
-        s_delta = b.dry ? 0.f : d;
-      }
-    }
-    __syncthreads();
-    const float d = scatter_scale<FORM>(s_delta);
-    if (d != 0.f || b.dry) {
-      for (int64_t base = beg + tid; base < end; base += (int64_t)T * U) {
-        // all U (idx, val) loads first: the REDs may alias them as far as the compiler knows,
-        // so interleaving would serialise one L2 round trip per entry
-        int32_t id[U];
-        float v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t k = base + (int64_t)u * T;
-          id[u] = k < end ? __ldcg(a.idx + k) : -1;
-          v[u] = k < end ? val_cg(a.val, k) : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (id[u] >= 0) red_add(a.sv + id[u], v[u] * d);
-      }
-    }
-  }
-}
-
-// ----------------------------------------------------------------------------------------------
-// Register-resident CTA kernel (first version, kept for comparison): E entries per thread held
-// in registers between the gather-dot and the scatter.
+// Register-resident CTA kernel: E entries per thread held in registers between the gather-dot and
+// the scatter (longer coordinates re-read the rest from L2 for the scatter).
 template <int FORM, int T, int E, bool WILD = false>
 __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
   constexpr int NW = T / 32;
@@ -314,18 +212,11 @@ __device__ __forceinline__ void red_add_v4(float *p, float4 v) {
                : "memory");
 }
 
-template <int T, bool SNAP>
-__device__ __forceinline__ void head_flush(float *sv, float *s_acc, float *s_w, int H, int dry) {
+template <int T>
+__device__ __forceinline__ void head_flush(float *sv, float *s_acc, int H, int dry) {
   float4 *a4 = reinterpret_cast<float4 *>(s_acc);
-  float4 *w4 = reinterpret_cast<float4 *>(s_w);
   for (int i = threadIdx.x; i < H / 4; i += T) {
     const float4 v = a4[i];
-    if (SNAP) {
-      // refresh the CTA's view of the head: L2 value (every flushed update) + own pending part,
-      // read BEFORE this CTA's RED of the pending part is issued (same thread, same address: ordered)
-      const float4 l = __ldcg(reinterpret_cast<const float4 *>(sv) + i);
-      w4[i] = make_float4(l.x + v.x, l.y + v.y, l.z + v.z, l.w + v.w);
-    }
     // dry probe: the pending array starts at -0.0f and the scatter adds +0.0f (non-negative values),
     // which turns a touched entry into +0.0f, so the probe flushes exactly the touched float4s
     const bool touched = dry ? (__float_as_uint(v.x) != 0x80000000u || __float_as_uint(v.y) != 0x80000000u ||
@@ -339,40 +230,34 @@ __device__ __forceinline__ void head_flush(float *sv, float *s_acc, float *s_w, 
   }
 }
 
-// Tail read (TS): TS = 0 gathers tail entries from sv itself; TS = 1 / 2 from the
-// read copy svr (refreshed before every slice launch, so never written during this kernel) with L2 /
-// L1-cached loads.  The lines gathered and the lines reduced are then disjoint, which the L2 serves
+// Shared-vector read of an entry of the row.  Head entries (id < H): L2 value + this
+// CTA's pending part, the L2 value from the rolling head copy svr[0, H) with HC, else from sv.  Tail
+// entries: from the read copy svr with TS (refreshed in rolling chunks / before every slice, never
+// reduced into), else from sv.  Gathered and reduced lines are then disjoint, which the L2 serves
 // ~35% faster (profiles/mix_bench_r1.txt: 84 -> 114 G gather+RED pairs/s).
-template <int TS>
-__device__ __forceinline__ float ld_tail(const EpochArgs &a, int32_t j) {
-  if (TS == 2) return __ldg(a.svr + j);
-  if (TS == 1) return __ldcg(a.svr + j);
-  return ld_sv(a.sv + j);
+template <int TS, bool HC>
+__device__ __forceinline__ float ld_entry(const EpochArgs &a, const float *s_acc, int H, int32_t j) {
+  if (j < H) return ld_sv((HC ? a.svr : a.sv) + j) + s_acc[j];
+  return ld_sv((TS ? a.svr : a.sv) + j);
 }
 
-// PF: thread 0 prefetches the next coordinate (ticket, permutation, offsets, model, norm, label)
-// while the CTA works on the current one and publishes it through shared memory, so the
-// ticket -> Feistel -> ptr -> x chain (three dependent round trips) leaves the per-row critical
-// path.  The prefetched coordinate reads nothing of the shared vector before its turn, so this adds
-// no staleness; x[c'] is current because this CTA is its only writer in the epoch (c10).
-template <int FORM, int T, int E, bool SNAP, int TS = 0, bool PF = false, bool HC = false>
+// Thread 0 prefetches the next coordinate (ticket, permutation, offsets, model, norm, label) while
+// the CTA works on the current one and publishes it through shared memory, so the ticket -> Feistel
+// -> ptr -> x chain (three dependent round trips) leaves the per-row critical path.  The prefetched
+// coordinate reads nothing of the shared vector before its turn, so this adds no staleness; x[c'] is
+// current because this CTA is its only writer in the epoch (c10).
+template <int FORM, int T, int E, int TS, bool HC>
 __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
   constexpr int NW = T / 32;
   extern __shared__ float4 s_dyn[];
   float *s_acc = reinterpret_cast<float *>(s_dyn);
-  float *s_w = s_acc + H;  // SNAP: the CTA's view of the head (refreshed at every flush)
   __shared__ float s_red[NW];
   __shared__ float s_delta;
-  __shared__ unsigned int s_ticket;
-  __shared__ int64_t s_cur[4];  // PF: coordinate (-1 = slice done), ptr[c], ptr[c + 1], its position t
-  __shared__ float s_cx[3];     // PF: x[c], norm[c], y[c]
+  __shared__ int64_t s_cur[4];  // coordinate (-1 = slice done), ptr[c], ptr[c + 1], its position t
+  __shared__ float s_cx[3];     // x[c], norm[c], y[c]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int i = tid; i < H; i += T) s_acc[i] = b.dry ? -0.f : 0.f;
-  if (SNAP) {
-    __syncthreads();
-    head_flush<T, true>(a.sv, s_acc, s_w, H, 0);  // initial view (nothing pending yet)
-  }
-  int64_t n_c = -1, n_beg = 0, n_end = 0, n_t = 0;  // PF (thread 0): the next coordinate
+  int64_t n_c = -1, n_beg = 0, n_end = 0, n_t = 0;  // thread 0: the next coordinate
   float n_x = 0.f, n_nrm = 0.f, n_y = 0.f;
   unsigned n_tk = 0;
   auto fetch = [&](unsigned tk) {
@@ -387,55 +272,42 @@ __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, Bin
     n_nrm = __ldg(a.norm + n_c);
     n_y = FORM == SCD_DUAL ? __ldg(a.y + n_c) : 0.f;
   };
-  if (PF && tid == 0) fetch(atomicAdd(b.counter, 1u));
+  if (tid == 0) fetch(atomicAdd(b.counter, 1u));
   int since = 0;
   for (;;) {
-    int64_t c, beg, end;
-    if (PF) {
-      if (tid == 0) {
-        s_cur[0] = n_c;
-        s_cur[1] = n_beg;
-        s_cur[2] = n_end;
-        s_cur[3] = n_t;
-        s_cx[0] = n_x;
-        s_cx[1] = n_nrm;
-        s_cx[2] = n_y;
-        if (n_c >= 0) n_tk = atomicAdd(b.counter, 1u);  // consumed after this row's gathers
-      }
-      __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
-      c = s_cur[0];
-      if (c < 0) break;
-      beg = s_cur[1];
-      end = s_cur[2];
-      if (HC && !b.dry && s_cur[3] % a.head_P == 0) {
-        // head copy (experiment): row position t refreshes chunk (t / head_P) mod (H / 1024) of svr[0, H)
-        const int64_t nchh = ((int64_t)H + T * 4 - 1) / (T * 4);
-        const int64_t ih = ((s_cur[3] / a.head_P) % nchh) * (T * 4) + (int64_t)tid * 4;
-        if (ih + 3 < H)
-          *reinterpret_cast<float4 *>(const_cast<float *>(a.svr) + ih) =
-              __ldcg(reinterpret_cast<const float4 *>(a.sv + ih));
-      }
-      if (TS && a.roll_R > 0 && !b.dry && s_cur[3] % a.roll_R == 0) {
-        // rolling tail copy: row position t refreshes chunk (t / roll_R) mod nchunks of
-        // svr from sv, so every tail entry of the copy is at most roll_R · nchunks positions old
-        // without any slice boundary (plain stores: a concurrent reader sees the old or the new value)
-        constexpr int64_t CH = (int64_t)T * 4;
-        const int64_t nch = (a.roll_hi - a.roll_lo + CH - 1) / CH;
-        const int64_t i = a.roll_lo + ((s_cur[3] / a.roll_R) % nch) * CH + (int64_t)tid * 4;
-        float *dst = const_cast<float *>(a.svr);
-        if (i + 3 < a.roll_hi)
-          *reinterpret_cast<float4 *>(dst + i) = __ldcg(reinterpret_cast<const float4 *>(a.sv + i));
-        else
-          for (int64_t q = i; q < a.roll_hi && q < i + 4; ++q) dst[q] = __ldcg(a.sv + q);
-      }
-    } else {
-      if (tid == 0) s_ticket = atomicAdd(b.counter, 1u);
-      __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
-      const int64_t t = b.lo + (int64_t)s_ticket;
-      if (t >= b.hi) break;
-      c = bin_coord(b, t);
-      beg = __ldg(a.ptr + c);
-      end = __ldg(a.ptr + c + 1);
+    if (tid == 0) {
+      s_cur[0] = n_c;
+      s_cur[1] = n_beg;
+      s_cur[2] = n_end;
+      s_cur[3] = n_t;
+      s_cx[0] = n_x;
+      s_cx[1] = n_nrm;
+      s_cx[2] = n_y;
+      if (n_c >= 0) n_tk = atomicAdd(b.counter, 1u);  // consumed after this row's gathers
+    }
+    __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
+    const int64_t c = s_cur[0];
+    if (c < 0) break;
+    const int64_t beg = s_cur[1], end = s_cur[2];
+    if (HC && !b.dry && s_cur[3] % a.head_P == 0) {
+      // head copy: row position t refreshes chunk (t / head_P) mod (H / 4T) of svr[0, H)
+      const int64_t nchh = ((int64_t)H + T * 4 - 1) / (T * 4);
+      const int64_t ih = ((s_cur[3] / a.head_P) % nchh) * (T * 4) + (int64_t)tid * 4;
+      if (ih + 3 < H)
+        *reinterpret_cast<float4 *>(const_cast<float *>(a.svr) + ih) = __ldcg(reinterpret_cast<const float4 *>(a.sv + ih));
+    }
+    if (TS && a.roll_R > 0 && !b.dry && s_cur[3] % a.roll_R == 0) {
+      // rolling tail copy: row position t refreshes chunk (t / roll_R) mod nchunks of
+      // svr from sv, so every tail entry of the copy is at most roll_R · nchunks positions old
+      // without any slice boundary (plain stores: a concurrent reader sees the old or the new value)
+      constexpr int64_t CH = (int64_t)T * 4;
+      const int64_t nch = (a.roll_hi - a.roll_lo + CH - 1) / CH;
+      const int64_t i = a.roll_lo + ((s_cur[3] / a.roll_R) % nch) * CH + (int64_t)tid * 4;
+      float *dst = const_cast<float *>(a.svr);
+      if (i + 3 < a.roll_hi)
+        *reinterpret_cast<float4 *>(dst + i) = __ldcg(reinterpret_cast<const float4 *>(a.sv + i));
+      else
+        for (int64_t q = i; q < a.roll_hi && q < i + 4; ++q) dst[q] = __ldcg(a.sv + q);
     }
     int32_t id[E];
     float v[E];
@@ -453,34 +325,15 @@ __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, Bin
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      if (id[e] >= 0) {
-        float w;
-        if (SNAP)
-          w = id[e] < H ? s_w[id[e]] + s_acc[id[e]] : ld_tail<TS>(a, id[e]);
-        else if (TS)
-          w = id[e] < H ? ld_sv((HC ? a.svr : a.sv) + id[e]) + s_acc[id[e]] : ld_tail<TS>(a, id[e]);
-        else
-          w = ld_sv(a.sv + id[e]) + (id[e] < H ? s_acc[id[e]] : 0.f);
-        acc = fmaf(w, v[e], acc);
-      }
+      if (id[e] >= 0) acc = fmaf(ld_entry<TS, HC>(a, s_acc, H, id[e]), v[e], acc);
     for (int64_t base = beg + (int64_t)T * E; base < end; base += (int64_t)T * E) {
 #pragma unroll 4
       for (int e = 0; e < E; ++e) {
         const int64_t k = base + (int64_t)e * T + tid;
-        if (k < end) {
-          const int32_t j = __ldcg(a.idx + k);
-          float w;
-          if (SNAP)
-            w = j < H ? s_w[j] + s_acc[j] : ld_tail<TS>(a, j);
-          else if (TS)
-            w = j < H ? ld_sv((HC ? a.svr : a.sv) + j) + s_acc[j] : ld_tail<TS>(a, j);
-          else
-            w = ld_sv(a.sv + j) + (j < H ? s_acc[j] : 0.f);
-          acc = fmaf(w, val_cg(a.val, k), acc);
-        }
+        if (k < end) acc = fmaf(ld_entry<TS, HC>(a, s_acc, H, __ldcg(a.idx + k)), val_cg(a.val, k), acc);
       }
     }
-    if (PF && tid == 0 && c >= 0) fetch(n_tk);  // next coordinate's chain overlaps reduce + scatter
+    if (tid == 0) fetch(n_tk);  // next coordinate's chain overlaps reduce + scatter
     acc = warp_sum(acc);
     if (lane == 0) s_red[wid] = acc;
     __syncthreads();
@@ -488,10 +341,8 @@ __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, Bin
       float s = lane < NW ? s_red[lane] : 0.f;
       s = warp_sum(s);
       if (lane == 0) {
-        const float xc = PF ? s_cx[0] : a.x[c];
-        const float nc = PF ? s_cx[1] : __ldg(a.norm + c);
-        const float yc = PF ? s_cx[2] : (FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f);
-        const float d = coord_delta<FORM>(s, xc, nc, yc, a.lam, a.lamN);
+        const float xc = s_cx[0];
+        const float d = coord_delta<FORM>(s, xc, s_cx[1], s_cx[2], a.lam, a.lamN);
         if (!b.dry) a.x[c] = xc + d;  // single writer per epoch (c10)
         s_delta = b.dry ? 0.f : d;
       }
@@ -529,125 +380,10 @@ __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, Bin
     if (++since == flush) {
       since = 0;
       __syncthreads();
-      head_flush<T, SNAP>(a.sv, s_acc, s_w, H, b.dry);
+      head_flush<T>(a.sv, s_acc, H, b.dry);
     }
   }
-  head_flush<T, false>(a.sv, s_acc, s_w, H, b.dry);  // after the exit barrier: every pending update is final
-}
-
-// ----------------------------------------------------------------------------------------------
-// Die-split CTA kernel (die.cu).  Every coordinate is processed by two CTAs, one on
-// each die, each over the part of the coordinate's entries whose shared-vector element is homed in
-// its own die's L2 (entries reordered at create: [ptr[c], mid[c]) die 0, [mid[c], ptr[c+1]) die 1).
-// CTAs of die d take tickets from die d's counter, so both dies walk the same permutation.  The two
-// partial dot products meet in a global slot (release/acquire, tagged with the launch); both CTAs
-// form dp = p0 + p1 in that order, hence the same Δ; the die-0 CTA is the single writer of x[c]
-// (c10) and each CTA scatters its own part.  The die-1 CTA reads x[c] before publishing its
-// partial, i.e. before die 0 can write it.  A CTA publishes before it waits, so the lowest
-// outstanding ticket always completes: no deadlock while every CTA is resident (grid <= occupancy).
-struct SplitArgs {
-  const int64_t *mid;
-  const int32_t *idx;
-  const float *val;  // nullptr = implicit values
-  const uint8_t *sm_die;
-  float *slot_p;
-  unsigned *slot_tag;
-  unsigned *err;
-  unsigned *counter1;  // die 1's ticket counter (die 0 uses BinArgs::counter)
-  unsigned tag;
-  int nosync;          // diagnostic only: no partner exchange (wrong Δ), isolates the rendezvous cost
-};
-
-__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned smid_now() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-
-template <int FORM, int T, int E>
-__global__ void __launch_bounds__(T, 4) k_epoch_split(EpochArgs a, BinArgs b, SplitArgs s) {
-  constexpr int NW = T / 32;
-  __shared__ float s_red[NW];
-  __shared__ float s_delta;
-  __shared__ unsigned int s_ticket;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int die = s.sm_die[smid_now()];  // a CTA never migrates
-  unsigned *counter = die == 0 ? b.counter : s.counter1;
-  for (;;) {
-    if (tid == 0) s_ticket = atomicAdd(counter, 1u);
-    __syncthreads();
-    const int64_t t = b.lo + (int64_t)s_ticket;
-    if (t >= b.hi) break;
-    const int64_t c = bin_coord(b, t);
-    const int64_t m = __ldg(s.mid + c);
-    const int64_t beg = die == 0 ? __ldg(a.ptr + c) : m;
-    const int64_t end = die == 0 ? m : __ldg(a.ptr + c + 1);
-    float xc = 0.f;
-    if (tid == 0) xc = a.x[c];  // before publishing (see above)
-    int32_t id[E];
-    float v[E];
-    float acc = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int64_t k = beg + (int64_t)e * T + tid;
-      if (k < end) {
-        id[e] = __ldcs(s.idx + k);
-        v[e] = val_cs(s.val, k);
-      } else {
-        id[e] = -1;
-        v[e] = 0.f;
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (id[e] >= 0) acc = fmaf(ld_sv(a.sv + id[e]), v[e], acc);
-    acc += dot_strided<8>(a.sv, s.idx, s.val, beg + (int64_t)T * E + tid, end, T);
-    acc = warp_sum(acc);
-    if (lane == 0) s_red[wid] = acc;
-    __syncthreads();
-    if (wid == 0) {
-      float p = lane < NW ? s_red[lane] : 0.f;
-      p = warp_sum(p);
-      if (lane == 0) {
-        const int64_t q = 2 * t;
-        if (s.nosync) {
-          s.slot_p[q + 1 - die] = 0.f;
-          s.slot_tag[q + 1 - die] = s.tag;
-        }
-        s.slot_p[q + die] = p;
-        st_release(s.slot_tag + q + die, s.tag);
-        unsigned spins = 0;
-        while (ld_acquire(s.slot_tag + q + (1 - die)) != s.tag) {
-          if (++spins > (1u << 26)) {  // partner never arrived: flag it, do not hang
-            atomicExch(s.err, 1u);
-            break;
-          }
-        }
-        const float po = __ldcg(s.slot_p + q + (1 - die));
-        const float dp = die == 0 ? p + po : po + p;
-        const float d = coord_delta<FORM>(dp, xc, __ldg(a.norm + c), FORM == SCD_DUAL ? __ldg(a.y + c) : 0.f,
-                                          a.lam, a.lamN);
-        if (die == 0 && !b.dry) a.x[c] = xc + d;  // single writer per epoch (c10)
-        s_delta = b.dry ? 0.f : d;
-      }
-    }
-    __syncthreads();
-    const float d = scatter_scale<FORM>(s_delta);
-    if (d != 0.f || b.dry) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      scatter_strided<8>(a.sv, s.idx, s.val, beg + (int64_t)T * E + tid, end, T, d);
-    }
-  }
+  head_flush<T>(a.sv, s_acc, H, b.dry);  // after the exit barrier: every pending update is final
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -703,126 +439,6 @@ __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
       scatter_regs<WILD, E>(a.sv, id, v, d);
       scatter_strided<8, WILD>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
     }
-  }
-}
-
-// ----------------------------------------------------------------------------------------------
-// Software-pipelined sub-warp kernel for short coordinates (criteo-shaped rows, 39 entries).
-// With a short coordinate the epoch is bound by its dependent round trips (ticket -> coordinate
-// -> offsets -> entries -> gathers -> delta -> scatter), and the staleness cap limits how many
-// coordinates may be in flight.  So each warp overlaps the next batch's loads with the current
-// batch's compute: while batch i gathers / reduces / scatters, batch i+1's offsets, scalars and
-// entries are already in flight, and batch i+2's coordinates are computed.  Only batch i reads
-// the shared vector, so prefetching does not add staleness.  Tickets are taken TB batches at a
-// time (one atomic per TB·32/G coordinates).
-template <int FORM, int G, int E, int TB>
-__global__ void __launch_bounds__(256) k_epoch_group_pipe(EpochArgs a, BinArgs b) {
-  constexpr int CPW = 32 / G;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane / G, gl = lane % G;
-  const unsigned FULL = 0xffffffffu;
-  unsigned int grab = 0, left = 0;
-  // warp-uniform: position of the next batch (or -1 when the slice is exhausted)
-  auto next_pos = [&]() -> int64_t {
-    if (left == 0) {
-      unsigned int g = 0;
-      if (lane == 0) g = atomicAdd(b.counter, (unsigned)(CPW * TB));
-      grab = __shfl_sync(FULL, g, 0);
-      left = TB;
-    }
-    const int64_t t = b.lo + (int64_t)grab + (int64_t)(TB - left) * CPW;
-    --left;
-    return t < b.hi ? t : -1;
-  };
-  // coordinate of this lane's group for the batch at position t (lanes < CPW evaluate the permutation)
-  auto coord_of = [&](int64_t t) -> int64_t {
-    int64_t cl = -1;
-    if (t >= 0 && lane < CPW && t + lane < b.hi) cl = bin_coord(b, (uint64_t)(t + lane));
-    return __shfl_sync(FULL, cl, sub);
-  };
-  // batch i (current) and i+1 (next) state
-  int64_t c_cur = coord_of(next_pos());
-  if (__all_sync(FULL, c_cur < 0)) return;
-  int64_t beg = 0, end = 0;
-  float xc = 0.f, nrm = 0.f, yc = 0.f;
-  if (c_cur >= 0) {
-    beg = __ldg(a.ptr + c_cur);
-    end = __ldg(a.ptr + c_cur + 1);
-    if (gl == 0) {
-      xc = a.x[c_cur];
-      nrm = __ldg(a.norm + c_cur);
-      if (FORM == SCD_DUAL) yc = __ldg(a.y + c_cur);
-    }
-  }
-  int32_t id[E];
-  float v[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int64_t k = beg + (int64_t)e * G + gl;
-    id[e] = k < end ? __ldcs(a.idx + k) : -1;
-    v[e] = k < end ? val_cs(a.val, k) : 0.f;
-  }
-  int64_t c_nxt = coord_of(next_pos());
-  while (!__all_sync(FULL, c_cur < 0)) {
-    // (a) offsets and scalars of batch i+1
-    int64_t nbeg = 0, nend = 0;
-    float nxc = 0.f, nnrm = 0.f, nyc = 0.f;
-    if (c_nxt >= 0) {
-      nbeg = __ldg(a.ptr + c_nxt);
-      nend = __ldg(a.ptr + c_nxt + 1);
-      if (gl == 0) {
-        nxc = a.x[c_nxt];
-        nnrm = __ldg(a.norm + c_nxt);
-        if (FORM == SCD_DUAL) nyc = __ldg(a.y + c_nxt);
-      }
-    }
-    // (b) gather-dot of batch i
-    float acc = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (id[e] >= 0) acc = fmaf(ld_sv(a.svg + id[e]), v[e], acc);
-    acc += dot_strided<8>(a.svg, a.idx, a.val, beg + (int64_t)G * E + gl, end, G);
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-    // (c) delta of batch i (group leader is the single writer of x[c], c10)
-    float d = 0.f;
-    if (c_cur >= 0 && gl == 0) {
-      d = coord_delta<FORM>(acc, xc, nrm, yc, a.lam, a.lamN);
-      if (!b.dry) a.x[c_cur] = xc + d;
-      if (b.dry) d = 0.f;
-    }
-    d = scatter_scale<FORM>(__shfl_sync(FULL, d, sub * G));
-    // (d) entries of batch i+1
-    int32_t nid[E];
-    float nv[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int64_t k = nbeg + (int64_t)e * G + gl;
-      nid[e] = k < nend ? __ldcs(a.idx + k) : -1;
-      nv[e] = k < nend ? val_cs(a.val, k) : 0.f;
-    }
-    // (e) scatter of batch i
-    if (d != 0.f || b.dry) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (id[e] >= 0) red_add(a.sv + id[e], v[e] * d);
-      scatter_strided<8>(a.sv, a.idx, a.val, beg + (int64_t)G * E + gl, end, G, d);
-    }
-    // (f) coordinates of batch i+2, rotate
-    const bool more = __any_sync(FULL, c_nxt >= 0);
-    const int64_t c_nn = more ? coord_of(next_pos()) : -1;
-    c_cur = c_nxt;
-    beg = nbeg;
-    end = nend;
-    xc = nxc;
-    nrm = nnrm;
-    yc = nyc;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      id[e] = nid[e];
-      v[e] = nv[e];
-    }
-    c_nxt = c_nn;
   }
 }
 
@@ -969,11 +585,10 @@ __global__ void __launch_bounds__(T) k_epoch_group_comb(EpochArgs a, BinArgs b) 
 // (hot.cu) the K most frequent entries get a slot and a private copy of the bin's indices is
 // re-encoded: id >= 0 = tail entry (shared-vector index), id < 0 = hot entry (slot = id & 0x7fffffff).
 // Each CTA keeps its pending updates of the hot entries in shared memory (s_pend, CAS-loop atomics:
-// the CTA's rows update them concurrently) and, with VIEW, a copy of their values refreshed at every
-// flush; the warps run their rows without any CTA barrier and meet every F row batches to flush
-// (one RED per touched hot entry) — so a hot line takes one RED per CTA per F batches instead of
-// one per row.  Pending (and, with VIEW, view age) are extra staleness, bounded by the schedule:
-// grid * rows per CTA * (1 + F * (VIEW ? 2 : 1)) <= cap.
+// the CTA's rows update them concurrently); the warps run their rows without any CTA barrier and
+// meet every F row batches to flush (one RED per touched hot entry) — so a hot line takes one RED
+// per CTA per F batches instead of one per row.  Pending updates are extra staleness, bounded by the
+// schedule: grid * rows per CTA * (1 + F) <= cap (plus the copy age and early gathers, below).
 struct HotArgs {
   const int32_t *idx;      // re-encoded entries of the bin's coordinates (same offsets as EpochArgs::ptr)
   const int32_t *hot_ids;  // [K]: shared-vector index of each hot slot
@@ -991,25 +606,20 @@ __global__ void k_hot_refresh(const float *sv, const int32_t *hot_ids, int K, fl
 // HC: the hot values are gathered from h.hc, a copy in slot order refreshed 32 slots at a time by the
 // warp whose ticket t has (t / rows per warp) mod P = 0, so the gathers leave the lines that take the
 // flush REDs; the copy's age (P · K/32 tickets) is counted in the window budget (hot_launch_shape).
-template <int FORM, int G, int E, bool VIEW, bool HC = false, bool TP = false, bool HP = false>
+template <int FORM, int G, int E, bool HC = false, bool TP = false, bool HP = false>
 __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
   constexpr int CPW = 32 / G;
   const unsigned FULL = 0xffffffffu;
   extern __shared__ float4 s_dyn[];
   float *s_pend = reinterpret_cast<float *>(s_dyn);  // [K] pending updates of the hot entries
-  float *s_aux = s_pend + h.K;                       // [K] VIEW: values; else: int32 shared-vector index
-  int32_t *s_hid = reinterpret_cast<int32_t *>(s_aux);
+  int32_t *s_hid = reinterpret_cast<int32_t *>(s_pend + h.K);  // [K] shared-vector index of each slot
   const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
   for (int i = threadIdx.x; i < h.K; i += blockDim.x) {
     s_pend[i] = b.dry ? -0.f : 0.f;
-    const int32_t j = __ldg(h.hot_ids + i);
-    if (VIEW)
-      s_aux[i] = ld_sv(a.sv + j);
-    else
-      s_hid[i] = j;
+    s_hid[i] = __ldg(h.hot_ids + i);
   }
   __syncthreads();
-  // Software pipeline (as in k_epoch_group_pipe): while batch i gathers, reduces and scatters, the
+  // Software pipeline: while batch i gathers, reduces and scatters, the
   // coordinates, offsets, scalars and entries of batch i+1 are already loaded.  Only batch i reads
   // the shared vector, so the prefetch adds no staleness.
   auto take = [&]() -> int64_t {  // warp-uniform: this lane's coordinate of the next batch, -1 = none
@@ -1094,7 +704,7 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
             w[e] = TP ? cur.tw[e] : ld_sv(a.sv + cur.id[e]);
           } else {
             const int sl = cur.id[e] & 0x7fffffff;
-            w[e] = (VIEW ? s_aux[sl] : (HP ? cur.tw[e] : (HC ? __ldcg(h.hc + sl) : ld_sv(a.sv + s_hid[sl])))) + s_pend[sl];
+            w[e] = (HP ? cur.tw[e] : (HC ? __ldcg(h.hc + sl) : ld_sv(a.sv + s_hid[sl]))) + s_pend[sl];
           }
         }
       }
@@ -1127,10 +737,9 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
       }
     }
     const bool any = __syncthreads_or(more);
-    for (int i = threadIdx.x; i < h.K; i += blockDim.x) {  // flush (and refresh the view)
+    for (int i = threadIdx.x; i < h.K; i += blockDim.x) {  // flush
       const float p = s_pend[i];
-      const int32_t j = VIEW ? __ldg(h.hot_ids + i) : s_hid[i];
-      if (VIEW) s_aux[i] = ld_sv(a.sv + j) + p;  // read before this CTA's RED: own pending counted once
+      const int32_t j = s_hid[i];
       // dry probe: pending starts at -0.0f and a touched slot becomes +0.0f (non-negative values)
       if (b.dry ? __float_as_uint(p) != 0x80000000u : p != 0.f) {
         red_add(a.sv + j, p);
@@ -1289,39 +898,20 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
 }
 
 // kernel table ---------------------------------------------------------------------------------
-constexpr int kCtaT = kLanesCta, kCtaE = 16, kStreamU = 4;
+constexpr int kCtaT = kLanesCta, kCtaE = 16;
 constexpr int kGrpE8 = 8, kGrpE32 = 16;
 constexpr int kClE = 8;
-
-// 8-lane bins: 0 = plain, 1 = software-pipelined, 2 = CTA-combining (default); SCD_GROUP_KERNEL
-constexpr int kCombT = 128, kCombS = 2048;
-inline int group_kind() {
-  static const int k = [] {
-    const char *e = getenv("SCD_GROUP_KERNEL");
-    if (!e) return 2;
-    std::string s(e);
-    return s == "plain" ? 0 : (s == "pipe" ? 1 : 2);
-  }();
-  return k;
-}
+constexpr int kCombT = 128, kCombS = 2048;  // CTA-combining kernel for 8-lane bins
 
 template <int FORM>
 void *kernel_for(int lanes, int plain) {
   switch (lanes) {
     case 8:
-      if (!plain && group_kind() == 2) return (void *)k_epoch_group_comb<FORM, 8, kCombT, kCombS>;
-      return (!plain && group_kind() == 1) ? (void *)k_epoch_group_pipe<FORM, 8, kGrpE8, 4> : (void *)k_epoch_group<FORM, 8, kGrpE8>;
-    case 16:
-      return group_kind() == 1 ? (void *)k_epoch_group_pipe<FORM, 16, 4, 4> : (void *)k_epoch_group<FORM, 16, 4>;
+      // CTA-combining by default; the plain 8-lane kernel when the bin's cap is below one CTA's batch
+      return plain ? (void *)k_epoch_group<FORM, 8, kGrpE8> : (void *)k_epoch_group_comb<FORM, 8, kCombT, kCombS>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
-    case kLanesCluster: return nullptr;  // cluster_kernel(): depends on the bin's cluster size
-    default: {
-      // register-resident kernel by default (measured equal-or-faster and half the coordinates in
-      // flight); SCD_CTA_KERNEL=stream selects the two-pass streaming variant
-      // read once per process (the launch shape at create and every launch must agree)
-      static const bool stream = getenv("SCD_CTA_KERNEL") && std::string(getenv("SCD_CTA_KERNEL")) == "stream";
-      return stream ? (void *)k_epoch_stream<FORM, kCtaT, kStreamU, 8> : (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
-    }
+    case kLanesCluster: return nullptr;  // cluster_kernel()
+    default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
   }
 }
 
@@ -1330,7 +920,6 @@ template <int FORM>
 void *kernel_wild(int lanes) {
   switch (lanes) {
     case 8: return (void *)k_epoch_group<FORM, 8, kGrpE8, true>;
-    case 16: return (void *)k_epoch_group<FORM, 16, 4, true>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32, true>;
     case kLanesCluster: return nullptr;
     default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE, true>;
@@ -1338,61 +927,35 @@ void *kernel_wild(int lanes) {
 }
 
 template <int FORM, bool WILD>
-void *cluster_kernel(int cl) {
-  switch (cl) {
-    case 2: return (void *)k_epoch_cluster<FORM, 2, kClusterThreads, kClE, WILD>;
-    case 4: return (void *)k_epoch_cluster<FORM, 4, kClusterThreads, kClE, WILD>;
-    case 16: {  // non-portable cluster size: opt in once per instantiation
-      void *fn = (void *)k_epoch_cluster<FORM, 16, kClusterThreads, kClE, WILD>;
-      cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      return fn;
-    }
-    default: return (void *)k_epoch_cluster<FORM, 8, kClusterThreads, kClE, WILD>;
-  }
+void *cluster_kernel() {
+  return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE, WILD>;
+}
+
+template <int FORM>
+void *hot_kernel(const scd_ctx *c) {
+  const bool hc = c->hot_copy > 0, tp = c->hot_tp;
+  if (hc && tp) return (void *)k_epoch_group_hot<FORM, 8, 8, true, true, true>;  // early hot gathers need the copy
+  if (hc) return (void *)k_epoch_group_hot<FORM, 8, 8, true, false, false>;
+  if (tp) return (void *)k_epoch_group_hot<FORM, 8, 8, false, true, false>;
+  return (void *)k_epoch_group_hot<FORM, 8, 8, false, false, false>;
 }
 
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
-  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view && c->hot_tp && c->hot_hp)
-    return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true, true, true>
-                                 : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true, true, true>;
-  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view && c->hot_tp)
-    return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true, true>
-                                 : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true, true>;
-  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild && c->hot_copy > 0 && !c->hot_view)
-    return c->form == SCD_PRIMAL ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false, true>
-                                 : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false, true>;
-  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild) {
-    if (c->form == SCD_PRIMAL)
-      return c->hot_view ? (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, true> : (void *)k_epoch_group_hot<SCD_PRIMAL, 8, 8, false>;
-    return c->hot_view ? (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, true> : (void *)k_epoch_group_hot<SCD_DUAL, 8, 8, false>;
-  }
+  if (b.hot > 0 && b.lanes == 8 && !c->opt.wild)
+    return c->form == SCD_PRIMAL ? hot_kernel<SCD_PRIMAL>(c) : hot_kernel<SCD_DUAL>(c);
   if (b.lanes == kLanesCluster) {
-    if (c->form == SCD_PRIMAL)
-      return c->opt.wild ? cluster_kernel<SCD_PRIMAL, true>(b.cl) : cluster_kernel<SCD_PRIMAL, false>(b.cl);
-    return c->opt.wild ? cluster_kernel<SCD_DUAL, true>(b.cl) : cluster_kernel<SCD_DUAL, false>(b.cl);
+    if (c->form == SCD_PRIMAL) return c->opt.wild ? cluster_kernel<SCD_PRIMAL, true>() : cluster_kernel<SCD_PRIMAL, false>();
+    return c->opt.wild ? cluster_kernel<SCD_DUAL, true>() : cluster_kernel<SCD_DUAL, false>();
   }
   if (c->opt.wild) return c->form == SCD_PRIMAL ? kernel_wild<SCD_PRIMAL>(b.lanes) : kernel_wild<SCD_DUAL>(b.lanes);
-  if (b.split && b.lanes == kLanesCta)
-    return c->form == SCD_PRIMAL ? (void *)k_epoch_split<SCD_PRIMAL, kCtaT, kCtaE>
-                                 : (void *)k_epoch_split<SCD_DUAL, kCtaT, kCtaE>;
-  if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && c->head_snap && c->form == SCD_DUAL)
-    return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true, 2>
-                             : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true, 1>;
-  if (b.head > 0 && b.lanes == kLanesCta && c->tail_snap && !c->head_snap && c->form == SCD_DUAL) {
-    if (c->head_pf && c->head_copy > 0 && c->tail_snap == 1)
-      return c->head_T == 512 ? (void *)k_epoch_cta_head<SCD_DUAL, 512, kCtaE, false, 1, true, true>
-                              : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true, true>;
-    if (c->head_pf)
-      return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 2, true>
-                               : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1, true>;
-    return c->tail_snap == 2 ? (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 2>
-                             : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false, 1>;
+  if (b.head > 0 && b.lanes == kLanesCta) {
+    // the read copies exist only for the dual (setup_tail_snap); the head copy needs the rolling tail copy
+    if (c->form == SCD_DUAL && c->tail_snap && c->head_copy > 0)
+      return (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, 1, true>;
+    if (c->form == SCD_DUAL && c->tail_snap) return (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, 1, false>;
+    return c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE, 0, false>
+                                 : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, 0, false>;
   }
-  if (b.head > 0 && b.lanes == kLanesCta)
-    return c->head_snap ? (c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE, true>
-                                                 : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, true>)
-                        : (c->form == SCD_PRIMAL ? (void *)k_epoch_cta_head<SCD_PRIMAL, kCtaT, kCtaE, false>
-                                                 : (void *)k_epoch_cta_head<SCD_DUAL, kCtaT, kCtaE, false>);
   return c->form == SCD_PRIMAL ? kernel_for<SCD_PRIMAL>(b.lanes, b.plain) : kernel_for<SCD_DUAL>(b.lanes, b.plain);
 }
 
@@ -1458,24 +1021,22 @@ int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t
 // C5 shard).  The grid is lowered (in steps of one CTA per SM, not below one per SM) until F >= 6
 // fits the budget.  SCD_HOT_T=256, SCD_HOT_F, SCD_HOT_CTAS (CTAs per SM) override (experiments).
 void hot_launch_shape(scd_ctx *c, Bin &b) {
-  void *fn = bin_kernel(c, b);
+  constexpr int T = 512;
   const size_t smem = 8 * (size_t)b.hot;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t rows = T / 8;
   int occ = 1;
-  const int T0 = getenv("SCD_HOT_T") && atoi(getenv("SCD_HOT_T")) == 256 ? 256 : 512;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T0, smem);
-  if (occ < 1) occ = 1;
-  if (const char *e = getenv("SCD_HOT_CTAS")) occ = std::max(1, std::min(occ, atoi(e)));
-  const int T = getenv("SCD_HOT_T") && atoi(getenv("SCD_HOT_T")) == 256 ? 256 : 512;
-  const int64_t k = c->hot_view ? 2 : 1, rows = T / 8;
+  {
+    void *fn = bin_kernel(c, b);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T, smem);
+    if (occ < 1) occ = 1;
+  }
   const int64_t need = (b.count + rows - 1) / rows;
   int64_t grid = std::min<int64_t>((int64_t)c->nsm * occ, std::max<int64_t>(need, 1));
-  const char *fe = getenv("SCD_HOT_F");
-  const int64_t min_grid = (int64_t)c->nsm * (T == 512 ? 1 : 2);
-  while (!fe && combine_window(c, b, grid * rows, k) < 6 && grid > min_grid) grid -= c->nsm;
-  int64_t F = std::max<int64_t>(1, std::min<int64_t>(64, combine_window(c, b, grid * rows, k)));
-  if (fe) F = std::max(1, atoi(fe));
-  if (!fe && F < 4) {  // too short a window to beat the CTA-combining kernel: use that instead
+  // lower the grid (whole CTAs per SM, not below one per SM) until a window of 6 batches fits
+  while (combine_window(c, b, grid * rows, 1) < 6 && grid > (int64_t)c->nsm) grid -= c->nsm;
+  const int64_t F = std::max<int64_t>(1, std::min<int64_t>(64, combine_window(c, b, grid * rows, 1)));
+  if (F < 4) {  // too short a window to beat the CTA-combining kernel: use that instead
     b.hot = 0;
     bin_launch_shape(c, b);
     return;
@@ -1485,31 +1046,27 @@ void hot_launch_shape(scd_ctx *c, Bin &b) {
   b.flush = (int)F;
   // Hot copy: the copy's age, P · K/32 warp tickets of rows/warp rows each, joins the window budget:
   // rows in flight · (1 + F + hp) + age <= budget, hp = 1 when the hot values are also gathered one
-  // step early (hot_hp: one more round of the rows in flight); F gives way (down to 4) until P >= 8
-  // fits.  SCD_HOT_COPY=0: off, =P: forced period; SCD_HOT_HP=0: no early hot gathers.
+  // step early (with the early tail gathers, hot_tp); F gives way (down to 4) until P >= 8 fits.
   c->hot_copy = 0;
-  c->hot_hp = !(getenv("SCD_HOT_HP") && atoi(getenv("SCD_HOT_HP")) == 0);
-  const char *hce = getenv("SCD_HOT_COPY");
-  if (!c->hot_view && !(hce && atoll(hce) == 0) && T == 512) {
-    const double budget = combine_budget(c, b);
-    const int64_t inflight = (int64_t)b.grid * rows, nch = (b.hot + 31) / 32, cpw = 32 / 8;
-    const double hp = c->hot_hp ? 1.0 : 0.0;
-    int64_t P = 0, f = F;
-    for (; f >= 4; --f) {
-      P = (int64_t)((budget - (double)inflight * (1.0 + hp + f)) / (double)(nch * cpw));
-      if (P >= 8) break;
-    }
-    if (hce) P = atoll(hce);
-    if (P >= 8 || hce) {
-      if (!c->hot_hc && cudaMalloc((void **)&c->hot_hc, sizeof(float) * (size_t)b.hot) != cudaSuccess) {
-        cudaGetLastError();
-        c->hot_hc = nullptr;
-        return;
-      }
-      c->hot_copy = std::max<int64_t>(1, P);
-      if (!hce) b.flush = (int)f;
-    }
+  const double budget = combine_budget(c, b);
+  const int64_t inflight = (int64_t)b.grid * rows, nch = (b.hot + 31) / 32, cpw = 32 / 8;
+  const double hp = c->hot_tp ? 1.0 : 0.0;
+  int64_t P = 0, f = F;
+  for (; f >= 4; --f) {
+    P = (int64_t)((budget - (double)inflight * (1.0 + hp + f)) / (double)(nch * cpw));
+    if (P >= 8) break;
   }
+  if (P >= 8) {
+    if (!c->hot_hc && cudaMalloc((void **)&c->hot_hc, sizeof(float) * (size_t)b.hot) != cudaSuccess) {
+      cudaGetLastError();
+      c->hot_hc = nullptr;
+      return;
+    }
+    c->hot_copy = P;
+    b.flush = (int)f;
+  }
+  // the early hot gathers read the copy: without it the kernel reads the hot values in their turn
+  c->hot_hp = c->hot_copy > 0 && c->hot_tp;
 }
 
 // Grid/block for a bin (used by build_schedule): persistent, sized to the SM count times the
@@ -1520,18 +1077,12 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   // caps fall back to the plain 8-lane kernel, and caps below 4 to one warp per coordinate.
   if (b.lanes == 8 && b.cap > 0 && b.cap < kCombT / 8) b.plain = 1;
   if (b.lanes == 8 && b.cap > 0 && b.cap < 4) b.lanes = 32;
-  if (c->opt.wild) {  // plain kernels only (no head / CTA combining, no die split)
+  if (c->opt.wild) {  // plain kernels only (no head / CTA combining)
     b.plain = 1;
-    b.head = b.split = 0;
+    b.head = 0;
   }
-  if (b.lanes != kLanesCta) b.head = b.split = 0;
-  if (b.split) b.head = 0;
-  if (b.lanes == kLanesCluster) {
-    // cluster size: large clusters split one very long coordinate over more SMs, small ones keep
-    // more coordinates in flight; SCD_CLUSTER = 2|4|8 overrides
-    const int env_cl = getenv("SCD_CLUSTER") ? atoi(getenv("SCD_CLUSTER")) : 0;
-    b.cl = (env_cl == 2 || env_cl == 4 || env_cl == 8 || env_cl == 16) ? env_cl : kClusterCtas;
-  }
+  if (b.lanes != kLanesCta) b.head = 0;
+  if (b.lanes == kLanesCluster) b.cl = kClusterCtas;
   if (b.hot > 0 && (b.lanes != 8 || c->opt.wild)) b.hot = 0;
   if (b.hot > 0) {
     hot_launch_shape(c, b);
@@ -1540,14 +1091,14 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   void *fn = bin_kernel(c, b);
   const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
-  const bool comb = (b.lanes == 8 && !b.plain && group_kind() == 2);  // fixed CTA size (kernel template)
-  int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : (b.head > 0 ? c->head_T : kCtaT)));
+  const bool comb = (b.lanes == 8 && !b.plain);  // fixed CTA size (kernel template)
+  int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : kCtaT));
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
   if (group && !comb && b.cap > 0 && b.cap * b.lanes < block) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
     if (block < 32) block = 32;
   }
-  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head * (c->head_snap ? 2 : 1) : 0;
+  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head : 0;
   if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
@@ -1568,18 +1119,8 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   b.block = block;
   if (b.head > 0) {
     // Pending head updates of `flush` coordinates per CTA are missed by other CTAs' reads, on top
-    // of the grid coordinates in flight: grid * (1 + flush * k) <= combined-update budget, k = 2
-    // with the shared-memory view (a read may also miss what others flushed since the CTA's last
-    // refresh).  SCD_HEAD_FLUSH overrides (experiments only).
-    const int64_t k = c->head_snap ? 2 : 1;
-    int64_t f = combine_window(c, b, b.grid, k);
-    if (const char *e = getenv("SCD_HEAD_FLUSH")) f = atoi(e);
-    if (f > 64) f = 64;
-    if (f < 2 && c->head_snap) {  // no room for the view: plain head kernel
-      c->head_snap = false;
-      bin_launch_shape(c, b);
-      return;
-    }
+    // of the grid coordinates in flight: grid * (1 + flush) <= combined-update budget (reading c25)
+    int64_t f = std::min<int64_t>(64, combine_window(c, b, b.grid, 1));
     if (f < 2) {  // no combining possible within the budget: plain CTA kernel
       b.head = 0;
       b.flush = 0;
@@ -1595,8 +1136,6 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
   void *fn = bin_kernel(c, b);
   int H = b.head, F = b.flush;
   void *args_head[] = {&a, &ba, &H, &F};
-  SplitArgs sa;
-  void *args_split[] = {&a, &ba, &sa};
   HotArgs ha;
   void *args_hot[] = {&a, &ba, &ha};
   void **args = args_head;
@@ -1609,22 +1148,8 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
     ha.P = (int)std::max<int64_t>(1, c->hot_copy);
     args = args_hot;
   }
-  if (b.split) {
-    sa.mid = c->split_mid;
-    sa.idx = c->split_idx;
-    sa.val = c->split_val;
-    sa.sm_die = c->sm_die;
-    sa.slot_p = c->slot_p;
-    sa.slot_tag = c->slot_tag;
-    sa.err = c->split_err;
-    sa.counter1 = ba.counter + kMaxBins * kMaxSlices;    // die 1's counter: same (slice, bin), second half
-    if (++c->launch_tag == 0) ++c->launch_tag;                  // 0 = never written
-    sa.tag = c->launch_tag;
-    sa.nosync = c->split_nosync ? 1 : 0;
-    args = args_split;
-  }
-  const size_t smem = b.hot > 0 ? 8 * (size_t)b.hot
-                     : (b.head > 0 ? sizeof(float) * (size_t)b.head * (c->head_snap ? 2 : 1) : 0);
+  const size_t smem = b.hot > 0 ? 8 * (size_t)b.hot : (b.head > 0 ? sizeof(float) * (size_t)b.head : 0);
+  if (smem >= 48 * 1024) SCD_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(b.block), args, smem, s));
   return SCD_OK;
 }
@@ -1663,8 +1188,6 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
   const int S = c->n_slices;
   const int64_t Q = (int64_t)S * nparts;  // slices of the whole epoch; this part runs S of them
   SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins * S, s));
-  if (c->die_split)
-    SCD_CK(c, cudaMemsetAsync(c->counters + kMaxBins * kMaxSlices, 0, sizeof(unsigned int) * kMaxBins * S, s));
   for (int sl = 0; sl < S; ++sl) {
     const int64_t q = (int64_t)part * S + sl;
     for (int i = 0; i < c->n_bins; ++i) {
@@ -1740,7 +1263,7 @@ scd_status tune_shared_layout(scd_ctx *c) {
   const int nl = 1 + kSvCandidates * kReps;
   std::vector<cudaEvent_t> ev(nl + 1);
   for (auto &e : ev) SCD_CK(c, cudaEventCreate(&e));
-  SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices, s));
+  SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins * kMaxSlices, s));
   SCD_CK(c, cudaEventRecord(ev[0], s));
   for (int l = 0; l < nl; ++l) {
     const int ci = l == 0 ? 0 : (l - 1) % kSvCandidates;
@@ -1754,7 +1277,7 @@ scd_status tune_shared_layout(scd_ctx *c) {
     ba.dry = 1;
     ba.counter = c->counters + l % (kMaxBins * kMaxSlices);
     if (l > 0 && l % (kMaxBins * kMaxSlices) == 0)
-      SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices, s));
+      SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins * kMaxSlices, s));
     scd_status st = launch_bin(c, b, a, ba, (int64_t)b.grid, s);
     if (st != SCD_OK) return st;
     SCD_CK(c, cudaEventRecord(ev[l + 1], s));
@@ -1769,7 +1292,7 @@ scd_status tune_shared_layout(scd_ctx *c) {
     best_of[ci] = std::min(best_of[ci], ms);
   }
   for (auto &e : ev) cudaEventDestroy(e);
-  SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices, s));
+  SCD_CK(c, cudaMemsetAsync(c->counters, 0, sizeof(unsigned int) * kMaxBins * kMaxSlices, s));
   int best = 0;
   c->n_probe = 0;
   for (int ci = 0; ci < kSvCandidates; ++ci) {

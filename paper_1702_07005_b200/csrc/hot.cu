@@ -98,14 +98,13 @@ scd_status setup_hot(scd_ctx *c) {
       c->hot_ids = nullptr;
     } else {
       int32_t *slot_of = reinterpret_cast<int32_t *>(cnt);  // reuse: n int32
-      // slots in shared-vector order (SCD_HOT_ORDER=freq: most frequent first): the top values of a
-      // frequency-ranked field are consecutive ids, so a warp's flush REDs over 32 consecutive slots
-      // coalesce into a few sector operations instead of 32 on the hottest lines
+      // slots in shared-vector order, not frequency order: the top values of a frequency-ranked field
+      // are consecutive ids, so a warp's flush REDs over 32 consecutive slots coalesce into a few
+      // sector operations instead of 32 on the hottest lines (profiles/hot_order_r1.txt)
       std::vector<int32_t> hid((size_t)kk);
       cudaMemcpyAsync(hid.data(), ids_sorted, sizeof(int32_t) * kk, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
-      const char *ord = getenv("SCD_HOT_ORDER");
-      if (!(ord && std::string(ord) == "freq")) std::sort(hid.begin(), hid.end());
+      std::sort(hid.begin(), hid.end());
       cudaMemcpyAsync(c->hot_ids, hid.data(), sizeof(int32_t) * kk, cudaMemcpyHostToDevice, s);
       cudaMemsetAsync(slot_of, 0xff, sizeof(int32_t) * n, s);
       k_hot_slots<<<grid_for(kk, 256), 256, 0, s>>>(c->hot_ids, (int)kk, slot_of);
@@ -123,20 +122,19 @@ scd_status setup_hot(scd_ctx *c) {
   SCD_CK(c, cudaStreamSynchronize(s));
   if (st != SCD_OK) return st;
   if (b.hot > 0) {
-    c->hot_view = getenv("SCD_HOT_VIEW") && atoi(getenv("SCD_HOT_VIEW")) == 1;
     // Tail prefetch: the next batch's non-hot values are gathered one step early, i.e. up to one more
     // round of the rows in flight old.  Like the webspam tail copy (reading c26), that is allowed when
     // the coupling through the non-hot entries alone bounds it: 2 x rows in flight <= cap_fraction x
-    // tau_tail (estimated from the re-encoded indices, hot entries excluded).  SCD_HOT_TP=0: off.
+    // tau_tail (estimated from the re-encoded indices, hot entries excluded).  The launch shape is
+    // computed twice: the rows in flight decide hot_tp, and hot_tp joins the window budget.
     c->hot_tp = false;
-    if (!(getenv("SCD_HOT_TP") && atoi(getenv("SCD_HOT_TP")) == 0)) {
-      if (scd_status st2 = estimate_tail_tau(c, b.list, b.count, 0, &c->hot_tail_tau, c->hot_idx); st2 != SCD_OK)
-        return st2;
-    }
+    if (scd_status st2 = estimate_tail_tau(c, b.list, b.count, 0, &c->hot_tail_tau, c->hot_idx); st2 != SCD_OK)
+      return st2;
     bin_launch_shape(c, b);
     if (b.hot > 0 && c->hot_tail_tau > 0) {
       const double inflight = (double)b.grid * (b.block / 8);
       c->hot_tp = 2.0 * inflight <= cap_fraction() * c->hot_tail_tau;
+      if (c->hot_tp) bin_launch_shape(c, b);
     }
   }
   return SCD_OK;

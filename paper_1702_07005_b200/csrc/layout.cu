@@ -269,9 +269,9 @@ static scd_status active_extent(scd_ctx *c, int64_t *out) {
 
 static scd_status setup_tail_snap(scd_ctx *c, int head) {
   c->tail_snap = 0;
-  const char *e = getenv("SCD_TAIL_SNAP");
+  const char *e = getenv("SCD_TAIL_SNAP");  // 0 = off, 1 = forced past the staleness rule (tests)
   const int mode = e ? atoi(e) : 1;
-  if (head <= 0 || (mode != 1 && mode != 2) || c->form != SCD_DUAL) return SCD_OK;
+  if (head <= 0 || mode != 1 || c->form != SCD_DUAL) return SCD_OK;
   const int64_t h = c->sv_active - 1;
   if (h < head) return SCD_OK;
   c->tail_lo = head;
@@ -396,21 +396,13 @@ scd_status build_schedule(scd_ctx *c) {
   // bin thresholds (entries per coordinate): (0,64] -> 8-lane groups, (64,1024] -> warps,
   // (1024,16384] -> one CTA, > 16384 -> one 8-CTA cluster per coordinate
   constexpr int NB = 4;
-  int lanes[NB] = {8, 32, kLanesCta, kLanesCluster};
-  if (const char *e = getenv("SCD_SHORT_LANES")) {  // tuning: lanes per short coordinate (8, 16 or 32)
-    const int l = atoi(e);
-    if (l == 8 || l == 16 || l == 32) lanes[0] = l;
-  }
+  const int lanes[NB] = {8, 32, kLanesCta, kLanesCluster};
   int head = 0;
   if (scd_status st = choose_head(c, &head); st != SCD_OK) return st;
   // with the head-combining CTA kernel the medium rows (64, 1024] join the CTA bin (dual only): a
   // separate warp-bin launch per slice is a latency-bound single wave (C3: 2.5% of the step for 0.7%
-  // of the entries); SCD_HEAD_MIN sets the shortest row of the CTA bin (default 65)
-  int64_t lim1 = 1024;
-  if (head > 0 && c->form == SCD_DUAL) {
-    lim1 = 64;
-    if (const char *e = getenv("SCD_HEAD_MIN")) lim1 = std::max<int64_t>(64, std::min<int64_t>(1024, atoll(e) - 1));
-  }
+  // of the entries)
+  const int64_t lim1 = head > 0 && c->form == SCD_DUAL ? 64 : 1024;
   // empty coordinates (any lim1)
   std::vector<int32_t> empty;
   for (int64_t i = 0; i < n; ++i)
@@ -421,15 +413,12 @@ scd_status build_schedule(scd_ctx *c) {
     SCD_CK(c, cudaMalloc((void **)&c->empty_list, sizeof(int32_t) * empty.size()));
     SCD_CK(c, cudaMemcpy(c->empty_list, empty.data(), sizeof(int32_t) * empty.size(), cudaMemcpyHostToDevice));
   }
-  c->head_snap = getenv("SCD_HEAD_SNAP") && atoi(getenv("SCD_HEAD_SNAP")) == 1;
   c->sv_active = c->n_shared;
   if (c->form == SCD_DUAL) {
     if (scd_status st = active_extent(c, &c->sv_active); st != SCD_OK) return st;
     c->sv_active = std::max<int64_t>(1, std::min(c->sv_active, c->n_shared));
   }
   if (scd_status st = setup_tail_snap(c, head); st != SCD_OK) return st;
-  c->head_pf = !(getenv("SCD_HEAD_PF") && atoi(getenv("SCD_HEAD_PF")) == 0);
-  c->head_T = getenv("SCD_HEAD_T") && atoi(getenv("SCD_HEAD_T")) == 512 ? 512 : 256;
   c->head_copy = 0;
   // one binning pass with the medium-row boundary lim1 (launch order: longest coordinates first)
   auto bin_pass = [&](int64_t l1) -> scd_status {
@@ -515,10 +504,8 @@ scd_status build_schedule(scd_ctx *c) {
       const bool forced = getenv("SCD_TAIL_SNAP") != nullptr;
       // either refreshed between slices (a slice within the bound) or, with one head bin, in rolling
       // chunks whose full sweep is within the bound (possible with a shorter sweep than a slice)
-      const bool roll_env_off = getenv("SCD_TAIL_ROLL") && atoi(getenv("SCD_TAIL_ROLL")) == 0;
-      const int64_t nch = (c->tail_hi - c->tail_lo + 4 * c->head_T - 1) / (4 * c->head_T);
-      const bool can_roll = c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf &&
-                            !c->head_snap && nch > 0 &&
+      const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
+      const bool can_roll = c->n_bins == 1 && S_env == 0 && nch > 0 &&
                             std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0) >= (double)nch;
       keep = forced || (c->opt.max_inflight == 0 && (slice_rows <= cap_fraction() * c->tail_tau || can_roll));
     }
@@ -530,13 +517,11 @@ scd_status build_schedule(scd_ctx *c) {
       // tail_roll-th row, so that one full sweep of the tail takes no more rows than a slice would
       // (cap_fraction · τ_tail and 1/8 of the bin), and the epoch needs no slice boundaries (each
       // costs a drain of the grid behind the longest rows: ~65 µs on C3).
-      // SCD_TAIL_ROLL=0: refresh between 8 slices instead.
+      // With several bins (or SCD_SLICES) the copy is refreshed between slices instead.
       c->tail_roll = 0;
-      const bool roll_env_off = getenv("SCD_TAIL_ROLL") && atoi(getenv("SCD_TAIL_ROLL")) == 0;
-      if (c->n_bins == 1 && S_env == 0 && !roll_env_off && c->tail_snap == 1 && c->head_pf && !c->head_snap &&
-          c->opt.max_inflight == 0) {
+      if (c->n_bins == 1 && S_env == 0 && c->opt.max_inflight == 0) {
         const Bin &B = c->bins[bi];
-        const int64_t nch = (c->tail_hi - c->tail_lo + 4 * c->head_T - 1) / (4 * c->head_T);
+        const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
         const double sweep = std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0);
         const int64_t R = nch > 0 ? (int64_t)(sweep / (double)nch) : 0;
         if (R >= 1) {
@@ -549,11 +534,10 @@ scd_status build_schedule(scd_ctx *c) {
       // in the last P · nchunks rows: that age joins the combined-update budget (reading c25),
       // rows in flight + deferred + age = grid · (1 + flush) + P · nchunks <= budget; the flush window
       // gives way (down to 2) until P >= 16 fits (a shorter period costs more in refresh traffic than
-      // it saves: profiles/head_copy_r1.txt).  SCD_HEAD_COPY=0: off, =P: forced period.
+      // it saves: profiles/head_copy_r1.txt).
       Bin &HB = c->bins[bi];
-      const char *hce = getenv("SCD_HEAD_COPY");
-      if (c->tail_roll > 0 && HB.head > 0 && !(hce && atoll(hce) == 0)) {
-        const int64_t nchh = (HB.head + 4 * c->head_T - 1) / (4 * c->head_T);
+      if (c->tail_roll > 0 && HB.head > 0) {
+        const int64_t nchh = (HB.head + 4 * kLanesCta - 1) / (4 * kLanesCta);
         const double budget = combine_budget(c, HB);
         int64_t P = 0;
         int f = HB.flush;
@@ -561,10 +545,9 @@ scd_status build_schedule(scd_ctx *c) {
           P = (int64_t)((budget - (double)HB.grid * (1.0 + f)) / (double)nchh);
           if (P >= 16) break;
         }
-        if (hce) P = atoll(hce);
-        if (P >= 16 || hce) {
-          c->head_copy = std::max<int64_t>(1, P);
-          if (!hce) HB.flush = f;
+        if (P >= 16) {
+          c->head_copy = P;
+          HB.flush = f;
         }
       }
     } else {
@@ -576,14 +559,13 @@ scd_status build_schedule(scd_ctx *c) {
   // cap (cap_fraction * τ_b), the whole launch may gather from a copy of the shared vector taken
   // just before it — the same block-Jacobi bound as the in-flight cap, with the whole slice counted
   // as in flight — so the lines gathered and the lines reduced are disjoint.  Plain
-  // kernels only; the copy refresh must stay small next to the slice's own traffic.  SCD_BIN_SNAP=0: off.
-  const bool snap_ok = !(getenv("SCD_BIN_SNAP") && atoi(getenv("SCD_BIN_SNAP")) == 0) && !c->opt.deterministic &&
-                       !c->opt.wild && c->opt.max_inflight == 0;
+  // kernels only; the copy refresh must stay small next to the slice's own traffic.
+  const bool snap_ok = !c->opt.deterministic && !c->opt.wild && c->opt.max_inflight == 0;
   bool any_snap = false;
   for (int i = 0; i < c->n_bins && snap_ok; ++i) {
     Bin &B = c->bins[i];
     B.snap = 0;
-    if (B.head > 0 || B.hot > 0 || B.split) continue;
+    if (B.head > 0 || B.hot > 0) continue;
     const double slice = (double)B.count / (double)c->n_slices;
     const double refresh_bytes = 8.0 * (double)c->n_shared, slice_bytes = 16.0 * (double)B.nnz / c->n_slices;
     // like the combined-update windows (combine_window, reading c25) a slice may also be at most 1/8
@@ -598,8 +580,8 @@ scd_status build_schedule(scd_ctx *c) {
     SCD_CK(c, cudaMalloc((void **)&c->svr, sizeof(float) * (size_t)c->n_shared));
     SCD_CK(c, cudaMemsetAsync(c->svr, 0, sizeof(float) * (size_t)c->n_shared, c->stream));
   }
-  // two ticket counters per (slice, bin): the second feeds die 1 of the die-split kernel
-  SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * 2 * kMaxBins * kMaxSlices));
+  // one ticket counter per (slice, bin)
+  SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * kMaxBins * kMaxSlices));
   return SCD_OK;
 }
 

@@ -58,8 +58,7 @@ class Info(C.Structure):
                 ("launches", C.c_int64), ("tau_star", C.c_double), ("inflight_cap", C.c_int64),
                 ("bin_cap", C.c_int64 * 4), ("bin_tau", C.c_double * 4), ("n_slices", C.c_int32),
                 ("sv_offset_bytes", C.c_int64), ("probe_best_ms", C.c_float), ("probe_worst_ms", C.c_float),
-                ("bin_head", C.c_int32 * 4), ("bin_flush", C.c_int32 * 4), ("bin_split", C.c_int32 * 4),
-                ("die_split", C.c_int32), ("n_die_sm", C.c_int32 * 2), ("die_lat", C.c_float * 2), ("split_nnz0", C.c_int64), ("bin_hot", C.c_int32 * 4),
+                ("bin_head", C.c_int32 * 4), ("bin_flush", C.c_int32 * 4), ("bin_hot", C.c_int32 * 4),
                 ("hot_cover", C.c_double), ("tail_snap", C.c_int32), ("tail_tau", C.c_double), ("bin_snap", C.c_int32 * 4), ("tail_roll", C.c_int64), ("head_copy", C.c_int64), ("hot_copy", C.c_int64), ("hot_tp", C.c_int32), ("hot_tail_tau", C.c_double), ("hot_hp", C.c_int32)]
 
 
@@ -247,14 +246,12 @@ class Solver:
         return dict(n_coord=inf.n_coord, n_shared=inf.n_shared, nnz=inf.nnz, n_nonempty=inf.n_nonempty,
                     launches=inf.launches, tau_star=inf.tau_star, inflight_cap=inf.inflight_cap,
                     n_slices=inf.n_slices, sv_offset_bytes=inf.sv_offset_bytes,
-                    probe_ms=(inf.probe_best_ms, inf.probe_worst_ms), die_split=bool(inf.die_split),
-                    n_die_sm=(inf.n_die_sm[0], inf.n_die_sm[1]), die_lat=(inf.die_lat[0], inf.die_lat[1]),
-                    split_nnz0=inf.split_nnz0, hot_cover=inf.hot_cover, tail_snap=inf.tail_snap,
+                    probe_ms=(inf.probe_best_ms, inf.probe_worst_ms), hot_cover=inf.hot_cover, tail_snap=inf.tail_snap,
                     tail_tau=inf.tail_tau, tail_roll=inf.tail_roll, head_copy=inf.head_copy, hot_copy=inf.hot_copy, hot_tp=inf.hot_tp, hot_tail_tau=inf.hot_tail_tau, hot_hp=inf.hot_hp,
                     bins=[dict(lanes=inf.bin_kind[i], count=inf.bin_count[i], nnz=inf.bin_nnz[i],
                                grid=inf.bin_grid[i], block=inf.bin_block[i], cap=inf.bin_cap[i],
                                tau=inf.bin_tau[i], head=inf.bin_head[i], flush=inf.bin_flush[i],
-                               split=inf.bin_split[i], hot=inf.bin_hot[i], snap=inf.bin_snap[i])
+                               hot=inf.bin_hot[i], snap=inf.bin_snap[i])
                           for i in range(nb)])
 
     def profile_read(self) -> list[tuple[float, int]]:

@@ -3,8 +3,7 @@
   * k_epoch_cta_head (default for the C3-shaped dual): each CTA combines its updates of the dense head
     of w̄ in shared memory and flushes them every `flush` rows; the extra staleness is bounded by the
     schedule (grid * (1 + flush) <= τ).
-  * k_epoch_split (opt-in, SCD_DIE_SPLIT=1): every row processed by one CTA per die over the entries
-    homed in that die's L2, partial dots exchanged through a global slot.
+  * k_epoch_group_hot (default for criteo-shaped one-hot rows): the measured hot set combined per CTA.
 
 Input: the first 20 000 rows of C3 (BASELINE configs[2]; row generation is independent per row, so
 the prefix is exactly C3's rows), 7.5e7 stored entries, ~19 000 rows in the CTA bin, with λ scaled so
@@ -63,8 +62,6 @@ def _converge(d, pr, hist):
 
 def test_head_kernel_schedule_and_convergence(c3p, monkeypatch):
     monkeypatch.delenv("SCD_HEAD", raising=False)
-    monkeypatch.delenv("SCD_HEAD_FLUSH", raising=False)
-    monkeypatch.delenv("SCD_DIE_SPLIT", raising=False)
     info = _converge(*c3p)
     cta = [b for b in info["bins"] if b["lanes"] == 256]
     assert cta, info
@@ -72,7 +69,6 @@ def test_head_kernel_schedule_and_convergence(c3p, monkeypatch):
     assert b["head"] == 8192 and b["flush"] >= 2, b
     # rows in flight + pending head updates of `flush` rows per CTA: bounded by the staleness bound
     assert b["grid"] * (1 + b["flush"]) <= b["tau"], b
-    assert not info["die_split"]
     # tail read copy: only while one slice of the bin stays within half the tail coupling's bound
     if info["tail_snap"]:
         assert b["count"] / info["n_slices"] <= 0.5 * info["tail_tau"], info
@@ -100,19 +96,6 @@ def test_head_kernel_off_matches_too(c3p, monkeypatch):
     monkeypatch.setenv("SCD_HEAD", "0")
     info = _converge(*c3p)
     assert all(b["head"] == 0 for b in info["bins"])
-
-
-def test_die_split_kernel_convergence(c3p, monkeypatch):
-    monkeypatch.setenv("SCD_DIE_SPLIT", "1")
-    d, pr, hist = c3p
-    info = _converge(d, pr, hist)
-    if not info["die_split"]:  # pragma: no cover - a single-die part
-        pytest.skip("no two-die split found by the probe")
-    n0, n1 = info["n_die_sm"]
-    assert n0 > 0 and n1 > 0 and n0 + n1 == torch.cuda.get_device_properties(0).multi_processor_count
-    assert info["die_lat"][1] > 1.25 * info["die_lat"][0]
-    assert 0 < info["split_nnz0"] < info["nnz"]
-    assert any(b["split"] for b in info["bins"])
 
 
 def test_wild_variant_loses_updates(c3p):

@@ -1,7 +1,7 @@
 """GPU-only per-epoch gaps of schedule variants at full size, compared with a recorded oracle run
 (tools/fullsize_band.py output).  Each variant runs in its own process (env knobs are read at create).
 
-  python tools/band_variants.py C4 6 "" "SCD_BIN_SNAP=0" "SCD_SLICES=16"
+  python tools/band_variants.py C4 6 "" "SCD_SLICES=16" "BV_MAXIN=32" "BV_DET=1"
 """
 import json
 import os

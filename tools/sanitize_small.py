@@ -68,18 +68,15 @@ assert np.array_equal(np.sort(scd.permutation(1, 2, 1000)), np.arange(1000))
 for form in ("dual", "primal"):
     print("wild", form, run(d, form, wild=True), flush=True)
 # webspam-shaped rows (C3 prefix, λN = 350 as in the full C3) put every row in the CTA bin with a grid
-# covering every SM: head-combining kernel, its shared-memory view, and the die-split kernel
+# covering every SM: head-combining kernel, with and without the per-slice tail read copy
 c3 = synth.gen_host(synth.CONFIGS["C3"].with_rows(1500))
 c3["lam"] = 350.0 / 1500
-for env in ({}, {"SCD_HEAD_SNAP": "1", "SCD_HEAD_FLUSH": "2"}, {"SCD_DIE_SPLIT": "1"},
-            {"SCD_HEAD_FLUSH": "2", "SCD_TAIL_SNAP": "1"}, {"SCD_HEAD_FLUSH": "2", "SCD_TAIL_SNAP": "1", "SCD_HEAD_PF": "0"},
-            {"SCD_HEAD_FLUSH": "2", "SCD_TAIL_SNAP": "2", "SCD_HEAD_SNAP": "1"}):
+for env in ({}, {"SCD_TAIL_SNAP": "1"}, {"SCD_TAIL_SNAP": "0"}):
     os.environ.update(env)
     s = scd.Solver(c3["ptr"], c3["idx"], c3["val"], 1500, c3["n_cols"], c3["y"], c3["lam"], "dual", seed=3)
     inf = s.info()
     s.close()
-    print("c3 prefix", env, inf["bins"][0], "die_split", inf["die_split"], "tail_snap", inf["tail_snap"],
-          run(c3, "dual"), flush=True)
+    print("c3 prefix", env, inf["bins"][0], "tail_snap", inf["tail_snap"], run(c3, "dual"), flush=True)
     for k in env:
         del os.environ[k]
 # rolling refresh of the tail copy (one head-kernel launch per epoch): needs a bin of >= 8 x 657 rows
@@ -89,10 +86,10 @@ s = scd.Solver(c3r["ptr"], c3r["idx"], c3r["val"], 20_000, c3r["n_cols"], c3r["y
 inf = s.info()
 s.close()
 print("c3 rolling", inf["bins"][0], "tail_roll", inf["tail_roll"], run(c3r, "dual"), flush=True)
-# criteo-shaped rows with λN = 2e5 (as in the 8-GPU shards): the hot-set kernel (and its view variant)
+# criteo-shaped rows with λN = 2e5 (as in the 8-GPU shards): the hot-set kernel, explicit and implicit values
 c5h = synth.gen_host(synth.CONFIGS["C5"].with_rows(1_000_000))
 c5h["lam"] = 0.2
-for env in ({}, {"SCD_HOT_VIEW": "1", "SCD_HOT_F": "4"}):
+for env in ({},):
     os.environ.update(env)
     s = scd.Solver(c5h["ptr"], c5h["idx"], c5h["val"], c5h["n_rows"], c5h["n_cols"], c5h["y"], c5h["lam"], "dual",
                    seed=3)
