@@ -110,6 +110,9 @@ typedef struct {
                              violates the optimality conditions.  Uses the plain kernels (no head
                              combining, no CTA combining).  0 = atomic (default, the paper's TPA-SCD). */
   const scd_collectives *collectives; /* host-side transport hooks instead of nccl_comm (NULL = NCCL) */
+  int32_t block_order;    /* short coordinates (<= 64 entries, the 8-lane bins) are visited in blocks of this many
+                             consecutive coordinates in a random block order (reading c28; their per-coordinate
+                             offsets, model, norm and label then share sectors); 0 = default (32), 1 = off */
 } scd_options;
 
 typedef struct scd_ctx scd_ctx;
@@ -250,6 +253,13 @@ void scd_destroy(scd_ctx *c);                    /* NULL-safe; syncs the stream;
 /* ---- integer artefacts (computed on the device; bit-exact with the oracle) ---- */
 /* host_out[j] = P_(seed,epoch,stream)(j) for j in [0, n): the keyed Feistel bijection of c8. */
 scd_status scd_permutation(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *host_out);
+/* Epoch visiting order in block order (reading c28: used for the short-coordinate bins): the
+ * n / blk full blocks of blk consecutive positions are permuted by P_(seed,epoch,stream) over the
+ * blocks, a block's coordinates are visited in turn, the last partial block comes last.  host_out[t]
+ * = coordinate at position t (int64, n entries).  blk = 1 is scd_permutation.  Errors:
+ * SCD_E_INVALID_ARG (n < 0, blk < 1, NULL output), SCD_E_CUDA.                                 */
+scd_status scd_block_permutation(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk,
+                                 int64_t *host_out);
 /* owner_out[c] (host) = worker owning coordinate c in [0, count) for k workers (c15). */
 scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_owner_out);
 /* Stable transpose CSR <-> CSC computed on the device.  in->mem says where the input lives;

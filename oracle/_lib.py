@@ -26,6 +26,7 @@ def lib():
         L.orc_perm_at.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, _I64, _I64]
         L.orc_permutation.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, _I64, _P]
         L.orc_partition.argtypes = [C.c_uint64, _I64, C.c_int32, _P]
+        L.orc_block_order.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, _I64, _I64, _P]
         L.orc_transpose.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P]
         L.orc_sq_norms.argtypes = [_I64, _P, _P, _P]
         L.orc_primal_epoch.argtypes = [_I64, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P, _I64, _P]
@@ -50,6 +51,15 @@ def permutation(seed: int, epoch: int, n: int, stream: int = 0) -> np.ndarray:
     """P_epoch over [0, n) (DESIGN.md c8), int64."""
     out = np.empty(max(n, 1), np.int64)
     lib().orc_permutation(seed & (2**64 - 1), epoch, stream, n, p(out))
+    return out[:n]
+
+
+def block_order(seed: int, epoch: int, n: int, blk: int, stream: int = 0) -> np.ndarray:
+    """Epoch visiting order in blocks of blk consecutive coordinates (DESIGN.md c28), int64."""
+    if blk < 1:
+        raise ValueError("blk must be >= 1")
+    out = np.empty(max(n, 1), np.int64)
+    lib().orc_block_order(seed & (2**64 - 1), epoch, stream, n, blk, p(out))
     return out[:n]
 
 

@@ -70,6 +70,18 @@ void orc_permutation(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, 
   for (int64_t j = 0; j < n; ++j) out[j] = orc_perm_at(seed, epoch, stream, n, j);
 }
 
+/* Block order of an epoch (reading c28, short coordinates): the n / blk full blocks of blk
+ * consecutive coordinates are visited in the order of the permutation over the blocks, the coordinates
+ * of a block in turn, the last partial block (n mod blk coordinates) at the end.  out[t] = coordinate
+ * visited at position t. */
+void orc_block_order(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk, int64_t *out) {
+  const int64_t nf = n / blk;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t tb = t / blk;
+    out[t] = tb < nf ? orc_perm_at(seed, epoch, stream, nf, tb) * blk + (t - tb * blk) : t;
+  }
+}
+
 /* Partition (Alg. 3 "Partition data by feature and distribute on the K workers", P:274;
  * random rows P:462).  DESIGN.md c15: a random permutation (stream 0x50415254, epoch 0)
  * cut into K contiguous blocks whose sizes differ by at most one (first count%K blocks

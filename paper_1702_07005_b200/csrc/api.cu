@@ -556,6 +556,25 @@ scd_status scd_permutation(uint64_t seed, uint32_t epoch, uint32_t stream, int64
   return st;
 }
 
+scd_status scd_block_permutation(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk,
+                                 int64_t *host_out) {
+  g_err.clear();
+  if (n < 0 || blk < 1 || (n > 0 && !host_out)) return fail(nullptr, SCD_E_INVALID_ARG, "bad n / blk / output");
+  if (n == 0) return SCD_OK;
+  int64_t *d = nullptr;
+  cudaError_t e = cudaMalloc((void **)&d, sizeof(int64_t) * (size_t)n);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "alloc");
+  scd_status st = launch_block_order_export(seed, epoch, stream, n, blk, d, 0);
+  if (st == SCD_OK) {
+    e = cudaMemcpy(host_out, d, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = cuda_fail(nullptr, e, "copy");
+  } else {
+    fail(nullptr, st, "block order kernel failed");
+  }
+  cudaFree(d);
+  return st;
+}
+
 scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_owner_out) {
   g_err.clear();
   if (count < 0 || k < 1 || (count > 0 && !host_owner_out)) return fail(nullptr, SCD_E_INVALID_ARG, "bad count / k");

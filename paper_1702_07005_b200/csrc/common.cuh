@@ -94,9 +94,11 @@ struct Bin {
   int snap = 0;              // 1 = every slice launch gathers from a copy of the shared vector taken just
                              // before it (the whole slice within the bin's staleness cap)
   int64_t count = 0, nnz = 0;
+  int64_t maxlen = 0;        // longest coordinate of the bin (stored entries)
   int32_t *list = nullptr;   // device, coordinate ids ascending
   int grid = 0, block = 0;
   uint32_t stream_id = 0;    // permutation stream = 1 + bin index
+  int64_t blk = 0;           // > 1: the epoch visits blocks of blk consecutive coordinates (reading c28)
   double ms = 0.0;           // profiling accumulator
   int64_t prof_launches = 0;
 };
@@ -235,6 +237,8 @@ void bin_launch_shape(scd_ctx *c, Bin &b);
 double combine_budget(const scd_ctx *c, const Bin &b);  // deferred-update budget of a bin (reading c25)
 double cap_fraction();  // in-flight cap as a fraction of a staleness bound (layout.cu)
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
+scd_status launch_block_order_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk,
+                                     int64_t *d_out, cudaStream_t s);
 scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);
 
 // hot.cu ---------------------------------------------------------------------------------------

@@ -47,6 +47,7 @@ struct EpochArgs {
 struct BinArgs {
   const int32_t *list;  // coordinate ids of the bin (ascending); nullptr = identity
   int64_t lo, hi;       // this launch processes permutation positions [lo, hi) of the bin
+  int64_t blk;          // > 1: block order (reading c28): perm permutes the count / blk full blocks
   unsigned int *counter;
   Perm perm;
   int dry;  // 1 = layout probe: full gather/scatter traffic, model untouched, scatter adds +0.0f
@@ -129,8 +130,18 @@ __device__ __forceinline__ void scatter_strided(float *sv, const int32_t *idx, c
   }
 }
 
+// Position t of the bin's epoch order -> coordinate.  Block order (blk > 1, reading c28): the full
+// blocks of blk consecutive coordinates of the bin are visited in the keyed permutation's order and
+// the coordinates of a block in turn; the last, partial block (count mod blk) comes last.  A bijection
+// on [0, count), so every coordinate is still visited exactly once per epoch.
 __device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
-  uint64_t j = perm_apply(b.perm, t);
+  uint64_t j;
+  if (b.blk > 1) {
+    const uint64_t blk = (uint64_t)b.blk, tb = t / blk;
+    j = tb < b.perm.n ? perm_apply(b.perm, tb) * blk + (t - tb * blk) : t;
+  } else {
+    j = perm_apply(b.perm, t);
+  }
   return b.list ? (int64_t)__ldg(b.list + j) : (int64_t)j;
 }
 
@@ -606,8 +617,10 @@ __global__ void k_hot_refresh(const float *sv, const int32_t *hot_ids, int K, fl
 // HC: the hot values are gathered from h.hc, a copy in slot order refreshed 32 slots at a time by the
 // warp whose ticket t has (t / rows per warp) mod P = 0, so the gathers leave the lines that take the
 // flush REDs; the copy's age (P · K/32 tickets) is counted in the window budget (hot_launch_shape).
-template <int FORM, int G, int E, bool HC = false, bool TP = false, bool HP = false>
-__global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
+// E: entries per lane (5 covers the 39-entry criteo rows at 8 lanes); IMP: implicit values (val =
+// NULL, NEXT-1: no value registers); T: threads of the one CTA per SM.
+template <int FORM, int G, int E, bool HC = false, bool TP = false, bool HP = false, bool IMP = false, int T = 512>
+__global__ void __launch_bounds__(T, 1) k_epoch_group_hot(EpochArgs a, BinArgs b, HotArgs h) {
   constexpr int CPW = 32 / G;
   const unsigned FULL = 0xffffffffu;
   extern __shared__ float4 s_dyn[];
@@ -619,14 +632,18 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
     s_hid[i] = __ldg(h.hot_ids + i);
   }
   __syncthreads();
-  // Software pipeline: while batch i gathers, reduces and scatters, the
-  // coordinates, offsets, scalars and entries of batch i+1 are already loaded.  Only batch i reads
-  // the shared vector, so the prefetch adds no staleness.
-  auto take = [&]() -> int64_t {  // warp-uniform: this lane's coordinate of the next batch, -1 = none
-    unsigned int t0 = 0;
-    if (lane == 0) t0 = atomicAdd(b.counter, (unsigned)CPW);
-    t0 = __shfl_sync(FULL, t0, 0);
-    if (b.lo + (int64_t)t0 >= b.hi) return -2;  // slice exhausted (uniform)
+  // Software pipeline, three batches deep: while batch i gathers, reduces and scatters, the entries
+  // of batch i+1 are loading (their offsets arrived during batch i-1) and the offsets and scalars of
+  // batch i+2 are loading, its ticket having been taken one batch earlier still (the ticket atomic's
+  // round trip was the largest single stall: profiles/ncu_c5_hot_r2.md).  Only batch i reads the
+  // shared vector (plus the early gathers of batch i+1, TP / HP, counted in the window budget), so
+  // the prefetches add no staleness; x[c] is current because this warp is its only writer (c10).
+  unsigned tk_pf = 0;  // lane 0: ticket of the next take(), obtained one batch ahead
+  if (lane == 0) tk_pf = atomicAdd(b.counter, (unsigned)CPW);
+  auto take = [&]() -> int64_t {  // warp-uniform: this lane's coordinate of the next batch, -2 = none
+    const unsigned int t0 = __shfl_sync(FULL, tk_pf, 0);
+    if (b.lo + (int64_t)t0 >= b.hi) return -2;  // slice exhausted (uniform); every later ticket is too
+    if (lane == 0) tk_pf = atomicAdd(b.counter, (unsigned)CPW);
     if (HC && !b.dry) {
       const int64_t tk = (b.lo + (int64_t)t0) / CPW;
       if (tk % h.P == 0) {
@@ -638,6 +655,10 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
     int64_t cl = -1;
     if (lane < CPW && b.lo + (int64_t)t0 + lane < b.hi) cl = bin_coord(b, b.lo + t0 + lane);
     return __shfl_sync(FULL, cl, sub);
+  };
+  struct Meta {
+    int64_t c, beg, end;
+    float xc, nrm, yc;
   };
   struct Batch {
     int64_t c;
@@ -657,43 +678,56 @@ __global__ void __launch_bounds__(512) k_epoch_group_hot(EpochArgs a, BinArgs b,
           q.tw[e] = __ldcg(h.hc + (q.id[e] & 0x7fffffff));  // HP: hot copy value one step early too
       }
   };
-  auto load = [&](Batch &q, int64_t c) {
-    q.c = c;
-    q.valid = 0;
-    q.xc = q.nrm = q.yc = 0.f;
-    int64_t beg = 0, end = 0;
+  auto load_meta = [&](Meta &m, int64_t c) {
+    m.c = c;
+    m.beg = m.end = 0;
+    m.xc = m.nrm = m.yc = 0.f;
     if (c >= 0) {
-      beg = __ldg(a.ptr + c);
-      end = __ldg(a.ptr + c + 1);
+      m.beg = __ldg(a.ptr + c);
+      m.end = __ldg(a.ptr + c + 1);
       if (gl == 0) {
-        q.xc = a.x[c];  // this warp is the single writer of x[c]: the prefetched value is current
-        q.nrm = __ldg(a.norm + c);
-        if (FORM == SCD_DUAL) q.yc = __ldg(a.y + c);
+        m.xc = a.x[c];
+        m.nrm = __ldg(a.norm + c);
+        if (FORM == SCD_DUAL) m.yc = __ldg(a.y + c);
       }
     }
+  };
+  auto load_idx = [&](Batch &q, const Meta &m) {
+    q.c = m.c;
+    q.xc = m.xc;
+    q.nrm = m.nrm;
+    q.yc = m.yc;
+    q.valid = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int64_t k = beg + (int64_t)e * G + gl;
+      const int64_t k = m.beg + (int64_t)e * G + gl;
       q.id[e] = 0;
       q.v[e] = 0.f;
-      if (k < end) {
+      if (k < m.end) {
         q.id[e] = __ldcs(h.idx + k);
-        q.v[e] = val_cs(a.val, k);
+        q.v[e] = IMP ? 1.f : val_cs(a.val, k);
         q.valid |= 1u << e;
       }
     }
   };
   Batch cur, nxt;
+  Meta m1;
   int64_t cn = take();
   bool more = cn != -2;  // warp-uniform: the warp holds a batch
-  if (more) load(cur, cn);
-  if (TP && more) tail_prefetch(cur);
+  if (more) {
+    load_meta(m1, cn);
+    load_idx(cur, m1);
+    if (TP) tail_prefetch(cur);
+  }
   for (;;) {
     for (int it = 0; it < h.F && more; ++it) {
-      // next batch: ticket + coordinates + entries (no shared-vector access)
+      // next batch: coordinates (ticket taken one batch ago) + offsets + entries (no shared-vector access)
       cn = take();
       const bool have_next = cn != -2;
-      if (have_next) load(nxt, cn);
+      if (have_next) {
+        load_meta(m1, cn);
+        load_idx(nxt, m1);
+      }
       // current batch: gather-dot
       float w[E];
 #pragma unroll
@@ -808,6 +842,12 @@ __global__ void k_empty_fix(EpochArgs a, const int32_t *list, int64_t n) {
 __global__ void k_perm_export(Perm p, int64_t n, int64_t *out) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
     out[j] = (int64_t)perm_apply(p, (uint64_t)j);
+}
+
+// the epoch order of a bin in block order (reading c28), through bin_coord itself (identity list)
+__global__ void k_block_order_export(BinArgs b, int64_t n, int64_t *out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = bin_coord(b, (uint64_t)t);
 }
 
 __global__ void k_partition_export(Perm p, int64_t count, int32_t k, int32_t *owner) {
@@ -931,10 +971,19 @@ void *cluster_kernel() {
   return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE, WILD>;
 }
 
+template <int FORM, int E, bool IMP>
+void *hot_kernel_fast() {
+  return (void *)k_epoch_group_hot<FORM, 8, E, true, true, true, IMP, 512>;
+}
+
 template <int FORM>
-void *hot_kernel(const scd_ctx *c) {
+void *hot_kernel(const scd_ctx *c, const Bin &b) {
   const bool hc = c->hot_copy > 0, tp = c->hot_tp;
-  if (hc && tp) return (void *)k_epoch_group_hot<FORM, 8, 8, true, true, true>;  // early hot gathers need the copy
+  if (hc && tp) {  // the default: early hot gathers from the copy; specialised on row length and values
+    const bool imp = c->val == nullptr, e5 = b.maxlen <= 40;
+    if (e5) return imp ? hot_kernel_fast<FORM, 5, true>() : hot_kernel_fast<FORM, 5, false>();
+    return imp ? hot_kernel_fast<FORM, 8, true>() : hot_kernel_fast<FORM, 8, false>();
+  }
   if (hc) return (void *)k_epoch_group_hot<FORM, 8, 8, true, false, false>;
   if (tp) return (void *)k_epoch_group_hot<FORM, 8, 8, false, true, false>;
   return (void *)k_epoch_group_hot<FORM, 8, 8, false, false, false>;
@@ -942,7 +991,7 @@ void *hot_kernel(const scd_ctx *c) {
 
 void *bin_kernel(const scd_ctx *c, const Bin &b) {
   if (b.hot > 0 && b.lanes == 8 && !c->opt.wild)
-    return c->form == SCD_PRIMAL ? hot_kernel<SCD_PRIMAL>(c) : hot_kernel<SCD_DUAL>(c);
+    return c->form == SCD_PRIMAL ? hot_kernel<SCD_PRIMAL>(c, b) : hot_kernel<SCD_DUAL>(c, b);
   if (b.lanes == kLanesCluster) {
     if (c->form == SCD_PRIMAL) return c->opt.wild ? cluster_kernel<SCD_PRIMAL, true>() : cluster_kernel<SCD_PRIMAL, false>();
     return c->opt.wild ? cluster_kernel<SCD_DUAL, true>() : cluster_kernel<SCD_DUAL, false>();
@@ -1021,7 +1070,11 @@ int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t
 // C5 shard).  The grid is lowered (in steps of one CTA per SM, not below one per SM) until F >= 6
 // fits the budget.  SCD_HOT_T=256, SCD_HOT_F, SCD_HOT_CTAS (CTAs per SM) override (experiments).
 void hot_launch_shape(scd_ctx *c, Bin &b) {
+  // the 768-thread kernel exists only in the default (hot copy + early gathers) configuration
+  // one 512-thread CTA per SM, 64 rows in flight per CTA (profiles/c5_shape_r2.txt: 768 threads are ~5%
+  // faster only with a combined-update budget of 1.25 τ, 16 lanes per row at 1024 threads 30% slower)
   constexpr int T = 512;
+  b.block = T;
   const size_t smem = 8 * (size_t)b.hot;
   const int64_t rows = T / 8;
   int occ = 1;
@@ -1198,7 +1251,8 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       ba.hi = b.count * (q + 1) / Q;
       if (ba.hi <= ba.lo) continue;
       ba.counter = c->counters + sl * kMaxBins + i;
-      ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.count);
+      ba.blk = b.blk;
+      ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.blk > 1 ? b.count / b.blk : b.count);
       ba.dry = 0;
       const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;  // coordinates per CTA (or cluster) per round
       const int unit = b.lanes == kLanesCluster ? b.cl : 1;
@@ -1273,7 +1327,8 @@ scd_status tune_shared_layout(scd_ctx *c) {
     ba.list = b.list;
     ba.lo = 0;
     ba.hi = probe;
-    ba.perm = make_perm(c->opt.seed ^ 0x5052424Full, 0xFFFFFFFEu, b.stream_id, b.count);
+    ba.blk = b.blk;
+    ba.perm = make_perm(c->opt.seed ^ 0x5052424Full, 0xFFFFFFFEu, b.stream_id, b.blk > 1 ? b.count / b.blk : b.count);
     ba.dry = 1;
     ba.counter = c->counters + l % (kMaxBins * kMaxSlices);
     if (l > 0 && l % (kMaxBins * kMaxSlices) == 0)
@@ -1322,6 +1377,18 @@ scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, in
                               cudaStream_t s) {
   Perm p = make_perm(seed, epoch, stream, n);
   k_perm_export<<<grid_for(n, 256), 256, 0, s>>>(p, n, d_out);
+  return cudaGetLastError() == cudaSuccess ? SCD_OK : SCD_E_CUDA;
+}
+
+scd_status launch_block_order_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk,
+                                     int64_t *d_out, cudaStream_t s) {
+  BinArgs b{};
+  b.list = nullptr;
+  b.lo = 0;
+  b.hi = n;
+  b.blk = blk;
+  b.perm = make_perm(seed, epoch, stream, blk > 1 ? n / blk : n);
+  k_block_order_export<<<grid_for(n, 256), 256, 0, s>>>(b, n, d_out);
   return cudaGetLastError() == cudaSuccess ? SCD_OK : SCD_E_CUDA;
 }
 

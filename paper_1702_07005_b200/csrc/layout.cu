@@ -424,7 +424,7 @@ scd_status build_schedule(scd_ctx *c) {
   auto bin_pass = [&](int64_t l1) -> scd_status {
     const int64_t lim[NB] = {64, l1, 16384, INT64_MAX};
     std::vector<int32_t> lists[NB];
-    int64_t nnzb[NB] = {0, 0, 0, 0};
+    int64_t nnzb[NB] = {0, 0, 0, 0}, maxb[NB] = {0, 0, 0, 0};
     for (int64_t i = 0; i < n; ++i) {
       const int64_t L = hp[(size_t)i + 1] - hp[(size_t)i];
       if (L == 0) continue;
@@ -432,6 +432,7 @@ scd_status build_schedule(scd_ctx *c) {
         if (L <= lim[b]) {
           lists[b].push_back((int32_t)i);
           nnzb[b] += L;
+          maxb[b] = std::max(maxb[b], L);
           break;
         }
     }
@@ -444,6 +445,7 @@ scd_status build_schedule(scd_ctx *c) {
       B.lanes = lanes[b];
       B.count = (int64_t)lists[b].size();
       B.nnz = nnzb[b];
+      B.maxlen = maxb[b];
       B.stream_id = 1u + (uint32_t)c->n_bins;
       if (B.count == n) {
         B.list = nullptr;  // identity: every coordinate is in this bin
@@ -459,6 +461,8 @@ scd_status build_schedule(scd_ctx *c) {
       double cap = cap_fraction() * B.tau;
       B.cap = c->opt.max_inflight > 0 ? (int64_t)c->opt.max_inflight : (int64_t)(cap < 1 ? 1 : (cap > 1e9 ? 1e9 : cap));
       B.head = B.lanes == kLanesCta ? head : 0;
+      // block order for the short-coordinate bin (reading c28): 16.7 -> 13.1 ms on a C5 shard
+      B.blk = B.lanes == 8 ? (c->opt.block_order > 0 ? c->opt.block_order : 32) : 0;
       bin_launch_shape(c, B);
       ++c->n_bins;
     }

@@ -48,7 +48,8 @@ class Options(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("n_global", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_comm", C.c_void_p), ("stream", C.c_void_p), ("deterministic", C.c_int32),
                 ("max_inflight", C.c_int32), ("recompute_every", C.c_int32), ("validate", C.c_int32),
-                ("profile", C.c_int32), ("wild", C.c_int32), ("collectives", C.POINTER(Collectives))]
+                ("profile", C.c_int32), ("wild", C.c_int32), ("collectives", C.POINTER(Collectives)),
+                ("block_order", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -66,7 +67,7 @@ _lib = None
 EXPORTS = ("scd_default_options", "scd_create", "scd_epoch", "scd_epoch_part", "scd_objective", "scd_duality_gap", "scd_aggregate",
            "scd_aggregate_group", "scd_evaluate_group", "scd_get_model", "scd_get_shared", "scd_set_model", "scd_recompute_shared",
            "scd_get_stream", "scd_get_info", "scd_profile_read", "scd_last_error", "scd_last_global_error",
-           "scd_status_string", "scd_struct_sizes", "scd_destroy", "scd_permutation", "scd_partition", "scd_transpose", "scd_renumber", "scd_libsvm_size", "scd_libsvm_read",
+           "scd_status_string", "scd_struct_sizes", "scd_destroy", "scd_permutation", "scd_block_permutation", "scd_partition", "scd_transpose", "scd_renumber", "scd_libsvm_size", "scd_libsvm_read",
            "scd_nccl_unique_id", "scd_nccl_comm_init", "scd_nccl_comm_destroy")
 
 
@@ -101,6 +102,7 @@ def lib():
             "scd_struct_sizes": (None, [P]),
             "scd_destroy": (None, [V]),
             "scd_permutation": (C.c_int, [C.c_uint64, U32, U32, I64, P]),
+            "scd_block_permutation": (C.c_int, [C.c_uint64, U32, U32, I64, I64, P]),
             "scd_partition": (C.c_int, [C.c_uint64, I64, I32, P]),
             "scd_transpose": (C.c_int, [C.POINTER(Matrix), P, P, P, C.c_int]),
             "scd_renumber": (C.c_int, [C.POINTER(Matrix), P, P, P, P, C.c_int]),
@@ -155,7 +157,7 @@ class Solver:
                  seed: int = 0, deterministic: bool = False, max_inflight: int = 0, n_global: int = 0,
                  rank: int = 0, world: int = 1, nccl_comm=None, stream=None, validate: bool = True,
                  profile: bool = False, recompute_every: int = 0, wild: bool = False,
-                 collectives: Collectives | None = None):
+                 collectives: Collectives | None = None, block_order: int = 0):
         L = lib()
         self._form = PRIMAL if form == "primal" else DUAL
         if form not in ("primal", "dual"):
@@ -183,6 +185,7 @@ class Solver:
         o.validate = int(validate)
         o.profile = int(profile)
         o.wild = int(wild)
+        o.block_order = int(block_order)
         if collectives is not None:  # borrowed by the context: kept alive with it
             o.collectives = C.pointer(collectives)
         h = C.c_void_p()
@@ -297,6 +300,12 @@ def evaluate_group(solvers) -> tuple[float, float, float]:
 def permutation(seed: int, epoch: int, n: int, stream: int = 0) -> np.ndarray:
     out = np.empty(max(n, 1), np.int64)
     _check(lib().scd_permutation(seed & (2**64 - 1), epoch, stream, n, out.ctypes.data))
+    return out[:n]
+
+
+def block_permutation(seed: int, epoch: int, n: int, blk: int, stream: int = 0) -> np.ndarray:
+    out = np.empty(max(n, 1), np.int64)
+    _check(lib().scd_block_permutation(seed & (2**64 - 1), epoch, stream, n, blk, out.ctypes.data))
     return out[:n]
 
 

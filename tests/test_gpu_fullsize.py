@@ -26,10 +26,19 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_1702_07005_b200 as scd  # noqa: E402
 
 GPU_EPOCHS = 5
+BAND = 1.25         # reading c27: measured 1.06-1.09 x the envelope maximum (C3, C4), 0.3-1.1 elsewhere
 ORACLE_EPOCHS = 6   # C3 oracle gap 1.2e-10 after 6 epochs (profiles/data/band_C3.json): P* certified to ~2e-10
 
 
-def _side_by_side(form: str, band: list[float], cfg=None, seed: int = 3, implicit: bool = False,
+def _envelope(name):
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"seq_envelope_{name}.json")) as f:
+        return json.load(f)
+
+
+def _side_by_side(form: str, band: float, envelope: str, cfg=None, seed: int = 3, implicit: bool = False,
                   gpu_epochs: int = GPU_EPOCHS, oracle_epochs: int = ORACLE_EPOCHS, gap_at: int = 3):
     cfg = cfg or synth.CONFIGS["C3"]
     d = synth.gen_device(cfg)
@@ -84,10 +93,20 @@ def _side_by_side(form: str, band: list[float], cfg=None, seed: int = 3, implici
     # the gap at the start is the closed form ||y||²/(2N) (dual G_D(0)) / ||Aᵀy||²/(2λN²) (primal G_P(0))
     g0_ref = 0.5 * float(pr.y @ pr.y) / N if form == "dual" else float(np.sum((A.T @ pr.y) ** 2)) / (2 * pr.lam * N * N)
     assert g0 == pytest.approx(g0_ref, rel=1e-9)
-    # per-epoch band against the sequential trajectory (reading c27), while above the fp32 floor
-    for t, (g, o) in enumerate(zip(gaps, orc)):
-        if o[2] > 1e-8 * g0:
-            assert g <= band[t] * o[2], (t + 1, g, o[2], band[t])
+    # per-epoch band against the sequential method (reading c27): any random visiting order is a valid
+    # Alg. 1 run, and the sequential gap per epoch varies with the order (tests/golden/seq_envelope_*.json,
+    # written by tools/seq_envelope.py from oracle/ only); the GPU must stay within `band` x the largest
+    # sequential gap of the recorded seeds, while above the fp32 floor
+    env = _envelope(envelope)
+    print("envelope", ["%.3e" % e for e in env["envelope_max"]])
+    print("ratio to envelope max", ["%.3f" % (g / e) for g, e in zip(gaps, env["envelope_max"])])
+    assert env["lambda"] == pytest.approx(cfg.lam) and str(seed) in env["seeds"]
+    # the recorded trajectory of this seed is the live oracle run's (same data, same order)
+    for o, e in zip(orc, env["seeds"][str(seed)]["gap"]):
+        assert o[2] == pytest.approx(e, rel=1e-6)
+    for t, g in enumerate(gaps[:len(env["envelope_max"])]):
+        if env["envelope_min"][t] > 1e-8 * g0:
+            assert g <= band * env["envelope_max"][t], (t + 1, g, env["envelope_max"][t], band)
     # north_star tolerances at full size: gap <= 1e-5 and the objective within 1e-5 of the optimum
     assert gaps[gap_at - 1] <= 1e-5, gaps
     assert Gstar <= 1e-8 and abs(Pg - Pstar) <= 1e-5 * abs(Pstar), (Pg, Pstar)
@@ -96,8 +115,8 @@ def _side_by_side(form: str, band: list[float], cfg=None, seed: int = 3, implici
 
 def test_c3_dual_full_size_against_oracle():
     """Bench schedule on C3 (k_epoch_cta_head, one launch per epoch): per-epoch gap within 1.25x of the
-    sequential fp64 SDCA (measured 0.82-1.10x, profiles/data/band_C3.json), optimum to 1e-5."""
-    A, alpha, wbar, info = _side_by_side("dual", [1.25] * GPU_EPOCHS)
+    sequential fp64 SDCA's envelope over 4 seeds (measured <= 1.07x), optimum to 1e-5."""
+    A, alpha, wbar, info = _side_by_side("dual", BAND, "C3")
     b = info["bins"][0]
     assert info["n_bins"] == 1 and b["head"] > 0 and info["tail_roll"] > 0, info  # the benchmarked kernel
     # shared-vector consistency on the active features (fp32 accumulation drift)
@@ -113,15 +132,12 @@ def test_c4_primal_full_size_against_oracle():
     """BASELINE configs[3] at K = 1: C3's matrix by feature (device stable transpose to CSC, 16.6 M
     columns of which 15.9 M empty, heavy columns on the cluster kernel), per-epoch band against the
     sequential fp64 SCD (reading c27) and the optimum to 1e-5; w = Aβ on sampled rows."""
-    A, beta, w, _ = _side_by_side("primal", C4_BAND, seed=4)
+    A, beta, w, _ = _side_by_side("primal", BAND, "C4", seed=4)
     u = A @ beta
     rng = np.random.default_rng(1)
     rows = rng.choice(A.shape[0], size=20000, replace=False)
     err = np.abs(w[rows] - u[rows]).max() / np.abs(u).max()
     assert err <= 1e-4, err
-
-
-C4_BAND = [1.5] * GPU_EPOCHS
 
 
 def test_c5_shard_full_size_against_oracle():
@@ -130,8 +146,8 @@ def test_c5_shard_full_size_against_oracle():
     (k_epoch_group_hot), beside the sequential fp64 SDCA on the same rows (values 1.0 stored
     explicitly): per-epoch band (reading c27), gap <= 1e-5 and the optimum to 1e-5."""
     cfg = synth.CONFIGS["C5"].with_rows(25_000_000)
-    A, alpha, wbar, info = _side_by_side("dual", [1.5] * 4, cfg=cfg, seed=5, implicit=True, gpu_epochs=4,
-                                         oracle_epochs=5, gap_at=4)
+    A, alpha, wbar, info = _side_by_side("dual", BAND, "C5s", cfg=cfg, seed=5, implicit=True, gpu_epochs=4,
+                                         oracle_epochs=6, gap_at=4)
     b = info["bins"][0]
     assert info["n_bins"] == 1 and b["lanes"] == 8 and b["hot"] > 0, info
     v = A.T @ alpha

@@ -43,6 +43,13 @@ def test_permutation_bit_exact(n):
         assert np.array_equal(scd.permutation(77, t, n, st), oracle.permutation(77, t, n, st))
 
 
+@pytest.mark.parametrize("n,blk", [(1, 32), (31, 32), (1000, 32), (1003, 8), (350_000, 32), (25_000_000, 32)])
+def test_block_permutation_bit_exact(n, blk):
+    """The short-coordinate bins' block order (reading c28), through the kernels' own bin_coord."""
+    for t in (1, 2):
+        assert np.array_equal(scd.block_permutation(9, t, n, blk, 1), oracle.block_order(9, t, n, blk, stream=1))
+
+
 @pytest.mark.parametrize("count,k", [(0, 3), (5, 2), (8, 8), (1000, 7), (680_715, 8)])
 def test_partition_bit_exact(count, k):
     assert np.array_equal(scd.partition(4, count, k), oracle.partition(4, count, k))

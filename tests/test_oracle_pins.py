@@ -384,6 +384,23 @@ def test_permutation_is_bijection(n):
         assert np.array_equal(np.sort(p), np.arange(n))
 
 
+@pytest.mark.parametrize("n,blk", [(0, 32), (1, 32), (31, 32), (32, 32), (1000, 32), (1003, 8), (5000, 1), (777, 777)])
+def test_block_order_is_a_bijection_of_whole_blocks(n, blk):
+    """Reading c28: the full blocks of blk consecutive coordinates are visited whole, in the order of
+    the permutation over the blocks; the partial block last; blk = 1 is the plain permutation."""
+    o = oracle.block_order(5, 3, n, blk, stream=1)
+    assert np.array_equal(np.sort(o), np.arange(n))
+    nf = n // blk
+    if blk == 1:
+        assert np.array_equal(o, oracle.permutation(5, 3, n, stream=1))
+    for b in range(nf):
+        blkv = o[b * blk:(b + 1) * blk]
+        assert blkv[0] % blk == 0 and np.array_equal(blkv, blkv[0] + np.arange(blk))
+    if nf > 1:
+        assert np.array_equal(o[:nf * blk:blk] // blk, oracle.permutation(5, 3, nf, stream=1))
+    assert np.array_equal(o[nf * blk:], np.arange(nf * blk, n))
+
+
 def test_permutation_depends_on_epoch_and_is_mixing():
     n = 4096
     ps = [oracle.permutation(99, t, n) for t in range(1, 41)]

@@ -8,6 +8,7 @@ input generator synth/); writes tests/golden/seq_envelope_<cfg>.json.
 
   python tools/seq_envelope.py C3 6 3 4 5 6      # dual, 6 epochs, seeds 3..6
   python tools/seq_envelope.py C4 5 4 5 6 7      # primal (C3's matrix by feature)
+  python tools/seq_envelope.py C5s 4 5 6 7 8     # dual, one 25 M-row shard of C5 (standalone, λ = 1e-3)
 """
 import json
 import os
@@ -27,21 +28,26 @@ def main():
 
     which, E, seeds = sys.argv[1], int(sys.argv[2]), [int(x) for x in sys.argv[3:]]
     t0 = time.perf_counter()
-    d = synth.gen_host(synth.CONFIGS["C3"])
+    if which == "C5s":  # one GPU's shard of C5 as a standalone dual problem (25 M rows, values 1)
+        d = synth.gen_host(synth.CONFIGS["C5"].with_rows(25_000_000))
+    else:
+        d = synth.gen_host(synth.CONFIGS["C3"])
     pr = solver.Problem.from_csr(d, csc=which == "C4")
+    del d
     A = pr.A()
     print(f"setup {time.perf_counter() - t0:.1f} s", flush=True)
-    out = {"config": which, "epochs": E, "form": "dual" if which == "C3" else "primal", "lambda": pr.lam,
+    dual = which != "C4"
+    out = {"config": which, "epochs": E, "form": "dual" if dual else "primal", "lambda": pr.lam,
            "what": "sequential fp64 oracle (oracle.c Alg. 1) per-epoch duality gap (ridge.*_report, from scratch) "
                    "for several epoch-permutation seeds, full-size BASELINE configs[2]/[3]", "seeds": {}}
     for seed in seeds:
-        if which == "C3":
+        if dual:
             x, sv, nrm = np.zeros(pr.N), np.zeros(pr.M), pr.row_norms()
         else:
             x, sv, nrm = np.zeros(pr.M), np.zeros(pr.N), pr.col_norms()
         gaps, Ps = [], []
         for t in range(1, E + 1):
-            if which == "C3":
+            if dual:
                 solver.dual_epoch(pr, x, sv, oracle.permutation(seed, t, pr.N), nrm)
                 P, D, G = ridge.dual_report(A, pr.y, pr.lam, x)
             else:

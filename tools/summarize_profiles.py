@@ -51,6 +51,7 @@ KEYS = [
     "lts__t_sectors_srcunit_ltcfabric.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "smsp__inst_executed_op_global_red.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -94,9 +95,19 @@ def ncu(rep, out_prefix, bytes_per_launch=None):
     open(out_prefix + ".md", "w").write("\n".join(md))
     json.dump(js, open(out_prefix + ".json", "w"), indent=1)
     if js:
-        json.dump(dict(source=os.path.basename(out_prefix) + ".json", kernel=js[0]["kernel"],
-                       dram_bytes_per_launch=js[0]["dram_bytes_per_launch"]),
-                  open(os.path.join(os.path.dirname(out_prefix), "ncu_traffic.json"), "w"), indent=1)
+        # per-kernel map (short name -> DRAM bytes per launch of the last capture), read by bench.py
+        tp = os.path.join(os.path.dirname(out_prefix), "ncu_traffic.json")
+        try:
+            cur = json.load(open(tp))
+        except Exception:
+            cur = {}
+        if "kernel" in cur:  # old single-kernel format
+            cur = {}
+        for r in js:
+            short = r["kernel"].split("<")[0].split("::")[-1].replace("void ", "").strip()
+            cur[short] = dict(source=os.path.basename(out_prefix) + ".json", kernel=r["kernel"],
+                              dram_bytes_per_launch=r["dram_bytes_per_launch"])
+        json.dump(cur, open(tp, "w"), indent=1)
     print("\n".join(md))
 
 
