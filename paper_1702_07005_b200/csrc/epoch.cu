@@ -48,6 +48,7 @@ struct BinArgs {
   const int32_t *list;  // coordinate ids of the bin (ascending); nullptr = identity
   int64_t lo, hi;       // this launch processes permutation positions [lo, hi) of the bin
   int64_t blk;          // > 1: block order (reading c28): perm permutes the count / blk full blocks
+  int zero;             // 0 at run time (ticket_async)
   unsigned int *counter;
   Perm perm;
   int dry;  // 1 = layout probe: full gather/scatter traffic, model untouched, scatter adds +0.0f
@@ -128,6 +129,17 @@ __device__ __forceinline__ void scatter_strided(float *sv, const int32_t *idx, c
     }
     scatter_regs<WILD, U>(sv, id, v, d);
   }
+}
+
+// Ticket atomic of one lane whose result is consumed later (a prefetch).  ptxas turns an atomicAdd
+// on a warp-uniform address into a warp-aggregated one whose result shuffle waits for the atomic right
+// away (profiles/ncu_c5_hot_r2b: 16% of the hot kernel's stall samples on that shuffle); an address it
+// cannot prove uniform (offset lane * b.zero, b.zero = 0 at run time) keeps the plain ATOMG, so the
+// round trip overlaps the work until the ticket is used.
+__device__ __forceinline__ unsigned ticket_async(const struct BinArgs &b, unsigned n) {
+  unsigned l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));  // opaque to the compiler (it knows the caller's lane)
+  return atomicAdd(b.counter + l * (unsigned)b.zero, n);
 }
 
 // Position t of the bin's epoch order -> coordinate.  Block order (blk > 1, reading c28): the full
@@ -283,7 +295,7 @@ __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, Bin
     n_nrm = __ldg(a.norm + n_c);
     n_y = FORM == SCD_DUAL ? __ldg(a.y + n_c) : 0.f;
   };
-  if (tid == 0) fetch(atomicAdd(b.counter, 1u));
+  if (tid == 0) fetch(ticket_async(b, 1u));
   int since = 0;
   for (;;) {
     if (tid == 0) {
@@ -294,7 +306,7 @@ __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, Bin
       s_cx[0] = n_x;
       s_cx[1] = n_nrm;
       s_cx[2] = n_y;
-      if (n_c >= 0) n_tk = atomicAdd(b.counter, 1u);  // consumed after this row's gathers
+      if (n_c >= 0) n_tk = ticket_async(b, 1u);  // consumed after this row's gathers
     }
     __syncthreads();  // also orders the previous coordinate's s_acc updates before this one's reads
     const int64_t c = s_cur[0];
@@ -632,18 +644,18 @@ __global__ void __launch_bounds__(T, 1) k_epoch_group_hot(EpochArgs a, BinArgs b
     s_hid[i] = __ldg(h.hot_ids + i);
   }
   __syncthreads();
-  // Software pipeline, three batches deep: while batch i gathers, reduces and scatters, the entries
-  // of batch i+1 are loading (their offsets arrived during batch i-1) and the offsets and scalars of
-  // batch i+2 are loading, its ticket having been taken one batch earlier still (the ticket atomic's
-  // round trip was the largest single stall: profiles/ncu_c5_hot_r2.md).  Only batch i reads the
-  // shared vector (plus the early gathers of batch i+1, TP / HP, counted in the window budget), so
-  // the prefetches add no staleness; x[c] is current because this warp is its only writer (c10).
+  // Software pipeline: while batch i gathers, reduces and scatters, the offsets, scalars and entries
+  // of batch i+1 are loading, its ticket taken one batch earlier still (ticket_async).  Only batch i
+  // reads the shared vector (plus the early gathers of batch i+1, TP / HP, counted in the window
+  // budget), so the prefetches add no staleness; x[c] is current because this warp is its only
+  // writer (c10).  A deeper pipeline (offsets two batches ahead) measured no faster
+  // (profiles/c5_shape_r2.txt).
   unsigned tk_pf = 0;  // lane 0: ticket of the next take(), obtained one batch ahead
-  if (lane == 0) tk_pf = atomicAdd(b.counter, (unsigned)CPW);
+  if (lane == 0) tk_pf = ticket_async(b, (unsigned)CPW);
   auto take = [&]() -> int64_t {  // warp-uniform: this lane's coordinate of the next batch, -2 = none
     const unsigned int t0 = __shfl_sync(FULL, tk_pf, 0);
     if (b.lo + (int64_t)t0 >= b.hi) return -2;  // slice exhausted (uniform); every later ticket is too
-    if (lane == 0) tk_pf = atomicAdd(b.counter, (unsigned)CPW);
+    if (lane == 0) tk_pf = ticket_async(b, (unsigned)CPW);
     if (HC && !b.dry) {
       const int64_t tk = (b.lo + (int64_t)t0) / CPW;
       if (tk % h.P == 0) {
@@ -1252,6 +1264,7 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       if (ba.hi <= ba.lo) continue;
       ba.counter = c->counters + sl * kMaxBins + i;
       ba.blk = b.blk;
+      ba.zero = 0;
       ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.blk > 1 ? b.count / b.blk : b.count);
       ba.dry = 0;
       const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;  // coordinates per CTA (or cluster) per round
@@ -1328,6 +1341,7 @@ scd_status tune_shared_layout(scd_ctx *c) {
     ba.lo = 0;
     ba.hi = probe;
     ba.blk = b.blk;
+    ba.zero = 0;
     ba.perm = make_perm(c->opt.seed ^ 0x5052424Full, 0xFFFFFFFEu, b.stream_id, b.blk > 1 ? b.count / b.blk : b.count);
     ba.dry = 1;
     ba.counter = c->counters + l % (kMaxBins * kMaxSlices);
