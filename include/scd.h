@@ -262,6 +262,14 @@ scd_status scd_block_permutation(uint64_t seed, uint32_t epoch, uint32_t stream,
                                  int64_t *host_out);
 /* owner_out[c] (host) = worker owning coordinate c in [0, count) for k workers (c15). */
 scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_owner_out);
+/* Stored-entry balanced partition of the n outer coordinates of a matrix (columns of a CSC for the
+ * primal, rows of a CSR for the dual) over k workers ("partition the coordinates
+ * in an intelligent way"; reading c29): coordinates in decreasing length, ties in the order
+ * of the partition permutation of scd_partition (same seed), dealt in snake order 0..k-1, k-1..0, ...
+ * ptr[n+1] is host or device memory (ptr_mem); host_owner_out[n] receives the worker of each
+ * coordinate.  Errors: SCD_E_INVALID_ARG, SCD_E_UNSUPPORTED (n > 2^31-1), SCD_E_OOM, SCD_E_CUDA.   */
+scd_status scd_partition_balanced(const int64_t *ptr, int64_t n, scd_mem ptr_mem, uint64_t seed, int32_t k,
+                                  int32_t *host_owner_out);
 /* Stable transpose CSR <-> CSC computed on the device.  in->mem says where the input lives;
  * out_mem where ptr_out[inner+1] / idx_out[nnz] / val_out[nnz] (caller-allocated) live.
  * Within each output outer index, entries appear in increasing input-outer order.

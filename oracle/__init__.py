@@ -18,4 +18,4 @@ hand values).  Parity unpinned (no paper values; invariants only): the permutati
 and transpose artefacts — see DESIGN.md §5.
 """
 from . import data, ridge, solver  # noqa: F401
-from ._lib import block_order, permutation, partition, transpose, sq_norms, perm_at  # noqa: F401
+from ._lib import block_order, permutation, partition, partition_balanced, transpose, sq_norms, perm_at  # noqa: F401

@@ -72,6 +72,26 @@ def partition(seed: int, count: int, k: int) -> np.ndarray:
     return out[:count]
 
 
+def partition_balanced(ptr, seed: int, k: int) -> np.ndarray:
+    """Stored-entry balanced partition (reading c29): the outer
+    coordinates sorted by decreasing length, ties by their position in the partition permutation
+    (stream 0x50415254, epoch 0, as in partition()), dealt in snake order 0..k-1, k-1..0, ...;
+    owner[c] for c in [0, n), int32."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    ptr = np.asarray(ptr, np.int64)
+    n = len(ptr) - 1
+    lens = np.diff(ptr)
+    pos = np.empty(n, np.int64)
+    pos[permutation(seed, 0, n, stream=0x50415254)] = np.arange(n)
+    order = np.lexsort((pos, -lens))  # primary key: length descending; then position
+    i = np.arange(n)
+    r, j = i // k, i % k
+    owner = np.empty(n, np.int32)
+    owner[order] = np.where(r % 2 == 1, k - 1 - j, j)
+    return owner
+
+
 def transpose(ptr, idx, val, n_inner: int):
     """Stable CSR<->CSC transpose; returns (optr int64, oidx int32, oval float32)."""
     ptr, idx, val = c64(ptr, np.int64), c64(idx, np.int32), c64(val, np.float32)

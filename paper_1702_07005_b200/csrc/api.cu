@@ -594,6 +594,34 @@ scd_status scd_partition(uint64_t seed, int64_t count, int32_t k, int32_t *host_
 }
 
 
+scd_status scd_partition_balanced(const int64_t *ptr, int64_t n, scd_mem ptr_mem, uint64_t seed, int32_t k,
+                                  int32_t *host_owner_out) {
+  g_err.clear();
+  if (!ptr || n < 0 || k < 1 || (n > 0 && !host_owner_out)) return fail(nullptr, SCD_E_INVALID_ARG, "bad ptr / n / k");
+  if (n == 0) return SCD_OK;
+  if (n > INT32_MAX) return fail(nullptr, SCD_E_UNSUPPORTED, "n > 2^31-1");
+  int64_t *dp = const_cast<int64_t *>(ptr);
+  int32_t *d_owner = nullptr;
+  cudaStream_t s = 0;
+  if (ptr_mem == SCD_MEM_HOST) {
+    if (cudaMalloc((void **)&dp, sizeof(int64_t) * (size_t)(n + 1)) != cudaSuccess) return fail(nullptr, SCD_E_OOM, "alloc");
+    cudaMemcpy(dp, ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice);
+  }
+  scd_status st = SCD_OK;
+  if (cudaMalloc((void **)&d_owner, sizeof(int32_t) * (size_t)n) != cudaSuccess) {
+    st = fail(nullptr, SCD_E_OOM, "alloc");
+  } else {
+    std::string err;
+    st = partition_balanced_device(dp, n, seed, k, d_owner, s, err);
+    if (st != SCD_OK) fail(nullptr, st, err);
+    if (st == SCD_OK && cudaMemcpy(host_owner_out, d_owner, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost) != cudaSuccess)
+      st = fail(nullptr, SCD_E_CUDA, "copy");
+  }
+  cudaFree(d_owner);
+  if (ptr_mem == SCD_MEM_HOST) cudaFree(dp);
+  return st;
+}
+
 scd_status scd_transpose(const scd_matrix *in, int64_t *ptr_out, int32_t *idx_out, float *val_out, scd_mem out_mem) {
   g_err.clear();
   // in->val == NULL (implicit values) transposes the pattern only; val_out is then ignored

@@ -239,6 +239,8 @@ double cap_fraction();  // in-flight cap as a fraction of a staleness bound (lay
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
 scd_status launch_block_order_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk,
                                      int64_t *d_out, cudaStream_t s);
+scd_status partition_balanced_device(const int64_t *ptr, int64_t n, uint64_t seed, int32_t k, int32_t *d_owner,
+                                     cudaStream_t s, std::string &err);
 scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);
 
 // hot.cu ---------------------------------------------------------------------------------------

@@ -589,6 +589,55 @@ scd_status build_schedule(scd_ctx *c) {
   return SCD_OK;
 }
 
+// nnz-balanced partition of the outer coordinates over k workers ("partition the
+// coordinates in an intelligent way"; reading c29).  Coordinates in order of decreasing length, ties in
+// the order of the partition permutation (stream kPartStream, epoch 0: the random partition of c15),
+// dealt to the workers in snake order 0..k-1, k-1..0, ...  Every worker's stored-entry count is then
+// within the longest coordinate of every other's (the random partition of c15 balances counts only).
+__global__ void k_bal_keys(const int64_t *ptr, int64_t n, Perm p, unsigned long long *keys, int32_t *ids) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = (int64_t)perm_apply(p, (uint64_t)i);
+    const int64_t len = ptr[c + 1] - ptr[c];
+    const unsigned long long inv = 0xFFFFFFFFull - (unsigned long long)(len < 0xFFFFFFFFll ? len : 0xFFFFFFFFll);
+    keys[i] = (inv << 32) | (unsigned long long)i;  // length descending, then position ascending
+    ids[i] = (int32_t)c;
+  }
+}
+
+__global__ void k_bal_deal(const int32_t *ids, int64_t n, int32_t k, int32_t *owner) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / k, j = i % k;
+    owner[ids[i]] = (int32_t)((r & 1) ? k - 1 - j : j);
+  }
+}
+
+scd_status partition_balanced_device(const int64_t *ptr, int64_t n, uint64_t seed, int32_t k, int32_t *d_owner,
+                                     cudaStream_t s, std::string &err) {
+  auto ck = [&](cudaError_t e, const char *what) {
+    if (e != cudaSuccess) err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaSuccess;
+  };
+  unsigned long long *keys = nullptr, *keys2 = nullptr;
+  int32_t *ids = nullptr, *ids2 = nullptr;
+  void *tmp = nullptr;
+  size_t tb = 0;
+  bool ok = ck(cudaMallocAsync((void **)&keys, sizeof(*keys) * n, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&keys2, sizeof(*keys2) * n, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&ids, sizeof(*ids) * n, s), "alloc") &&
+            ck(cudaMallocAsync((void **)&ids2, sizeof(*ids2) * n, s), "alloc");
+  if (ok) {
+    k_bal_keys<<<grid_for(n, 256), 256, 0, s>>>(ptr, n, make_perm(seed, 0u, kPartStream, n), keys, ids);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, ids, ids2, n, 0, 64, s);
+    ok = ck(cudaMallocAsync(&tmp, tb, s), "alloc sort tmp") &&
+         ck(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, ids, ids2, n, 0, 64, s), "sort");
+    if (ok) k_bal_deal<<<grid_for(n, 256), 256, 0, s>>>(ids2, n, k, d_owner);
+    ok = ok && ck(cudaGetLastError(), "partition kernels");
+  }
+  for (void *q : {(void *)keys, (void *)keys2, (void *)ids, (void *)ids2, tmp})
+    if (q) cudaFreeAsync(q, s);
+  return ok ? SCD_OK : SCD_E_CUDA;
+}
+
 // Stable transpose on the device: stable radix sort of (inner index -> entry position), then
 // gather of the outer index and value.  Equal keys keep input order (increasing outer index).
 scd_status transpose_device(const int64_t *ptr, const int32_t *idx, const float *val, int64_t outer, int64_t inner,

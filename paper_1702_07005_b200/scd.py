@@ -67,7 +67,7 @@ _lib = None
 EXPORTS = ("scd_default_options", "scd_create", "scd_epoch", "scd_epoch_part", "scd_objective", "scd_duality_gap", "scd_aggregate",
            "scd_aggregate_group", "scd_evaluate_group", "scd_get_model", "scd_get_shared", "scd_set_model", "scd_recompute_shared",
            "scd_get_stream", "scd_get_info", "scd_profile_read", "scd_last_error", "scd_last_global_error",
-           "scd_status_string", "scd_struct_sizes", "scd_destroy", "scd_permutation", "scd_block_permutation", "scd_partition", "scd_transpose", "scd_renumber", "scd_libsvm_size", "scd_libsvm_read",
+           "scd_status_string", "scd_struct_sizes", "scd_destroy", "scd_permutation", "scd_block_permutation", "scd_partition", "scd_partition_balanced", "scd_transpose", "scd_renumber", "scd_libsvm_size", "scd_libsvm_read",
            "scd_nccl_unique_id", "scd_nccl_comm_init", "scd_nccl_comm_destroy")
 
 
@@ -104,6 +104,7 @@ def lib():
             "scd_permutation": (C.c_int, [C.c_uint64, U32, U32, I64, P]),
             "scd_block_permutation": (C.c_int, [C.c_uint64, U32, U32, I64, I64, P]),
             "scd_partition": (C.c_int, [C.c_uint64, I64, I32, P]),
+            "scd_partition_balanced": (C.c_int, [P, I64, C.c_int, C.c_uint64, I32, P]),
             "scd_transpose": (C.c_int, [C.POINTER(Matrix), P, P, P, C.c_int]),
             "scd_renumber": (C.c_int, [C.POINTER(Matrix), P, P, P, P, C.c_int]),
             "scd_libsvm_size": (C.c_int, [C.c_char_p, I64, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
@@ -313,6 +314,15 @@ def partition(seed: int, count: int, k: int) -> np.ndarray:
     out = np.empty(max(count, 1), np.int32)
     _check(lib().scd_partition(seed & (2**64 - 1), count, k, out.ctypes.data))
     return out[:count]
+
+
+def partition_balanced(ptr, seed: int, k: int) -> np.ndarray:
+    """Stored-entry balanced partition of the outer coordinates of ptr (scd_partition_balanced)."""
+    p, mp, kp = _buf(ptr, np.int64)
+    n = (len(kp) if mp == MEM_HOST else kp.numel()) - 1
+    out = np.empty(max(n, 1), np.int32)
+    _check(lib().scd_partition_balanced(p, n, mp, seed & (2**64 - 1), k, out.ctypes.data))
+    return out[:n]
 
 
 def transpose(ptr, idx, val, n_rows: int, n_cols: int, layout: str = "csr"):

@@ -43,6 +43,17 @@ def test_permutation_bit_exact(n):
         assert np.array_equal(scd.permutation(77, t, n, st), oracle.permutation(77, t, n, st))
 
 
+def test_partition_balanced_bit_exact():
+    """scd_partition_balanced (device sort + snake deal) against the oracle's definition (reading c29):
+    C3's columns (16.6 M, power-law lengths, 15.9 M empty) and a small ragged case."""
+    d = synth.gen_host(synth.CONFIGS["C3"].with_rows(3000))
+    cp, _, _ = oracle.transpose(d["ptr"], d["idx"], d["val"], d["n_cols"])
+    for k in (1, 2, 8):
+        assert np.array_equal(scd.partition_balanced(cp, 4, k), oracle.partition_balanced(cp, 4, k))
+    ptr = np.concatenate([[0], np.cumsum([5, 1, 4, 2, 3, 0])]).astype(np.int64)
+    assert scd.partition_balanced(torch.from_numpy(ptr).cuda(), 3, 2).tolist() == [0, 0, 1, 0, 1, 1]
+
+
 @pytest.mark.parametrize("n,blk", [(1, 32), (31, 32), (1000, 32), (1003, 8), (350_000, 32), (25_000_000, 32)])
 def test_block_permutation_bit_exact(n, blk):
     """The short-coordinate bins' block order (reading c28), through the kernels' own bin_coord."""

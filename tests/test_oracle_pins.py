@@ -401,6 +401,27 @@ def test_block_order_is_a_bijection_of_whole_blocks(n, blk):
     assert np.array_equal(o[nf * blk:], np.arange(nf * blk, n))
 
 
+@pytest.mark.parametrize("k", [1, 2, 3, 8])
+def test_partition_balanced_invariants(k):
+    """Reading c29: every coordinate gets one owner; counts differ by at most one; each worker's stored
+    entries are within one longest coordinate of every other's (snake dealing of decreasing lengths)."""
+    rng = np.random.default_rng(k)
+    lens = np.concatenate([rng.zipf(1.6, 3000).clip(1, 5000), np.zeros(57, np.int64)])
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    own = oracle.partition_balanced(ptr, 11, k)
+    assert own.min() >= 0 and own.max() < k
+    cnt = np.bincount(own, minlength=k)
+    assert cnt.max() - cnt.min() <= 1
+    load = np.bincount(own, weights=lens, minlength=k)
+    assert load.max() - load.min() <= lens.max()
+
+
+def test_partition_balanced_hand_example():
+    """Lengths 5,1,4,2,3,0 over k = 2: sorted 5,4,3,2,1,0 (coordinates 0,2,4,3,1,5) dealt 0,1,1,0,0,1."""
+    ptr = np.concatenate([[0], np.cumsum([5, 1, 4, 2, 3, 0])]).astype(np.int64)
+    assert oracle.partition_balanced(ptr, 3, 2).tolist() == [0, 0, 1, 0, 1, 1]
+
+
 def test_permutation_depends_on_epoch_and_is_mixing():
     n = 4096
     ps = [oracle.permutation(99, t, n) for t in range(1, 41)]

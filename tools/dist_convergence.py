@@ -47,7 +47,7 @@ def col_shards(p, i, v, owner, K):
 PARTS = int(os.environ.get("DIST_PARTS", "1"))  # > 1: sub-epoch rounds (scd_epoch_part)
 
 
-def run(solvers, mode, rounds, n_shared, stop=1e-6):
+def run(solvers, mode, rounds, n_shared, stop=float(os.environ.get("DIST_STOP", "1e-6"))):
     recs = []
     for r in range(1, rounds * PARTS + 1):
         ms = []
@@ -84,8 +84,15 @@ def main():
         del d
         torch.cuda.empty_cache()
         for K in [k for k in (1, 2, 4, 8) if k <= kmax]:
-            owner = torch.from_numpy(scd.partition(4, cfg.n_cols, K).astype(np.int64)).cuda()
+            # DIST_PART=balanced: stored-entry balanced partition (reading c29, NEXT-3); default: random (c15)
+            if os.environ.get("DIST_PART") == "balanced":
+                owner = torch.from_numpy(scd.partition_balanced(p, 4, K).astype(np.int64)).cuda()
+            else:
+                owner = torch.from_numpy(scd.partition(4, cfg.n_cols, K).astype(np.int64)).cuda()
             shards = col_shards(p, i, v, owner, K)
+            nnz_k = [int(sp[-1].item()) for sp, _, _, _ in shards]
+            print(f"K={K} partition {os.environ.get('DIST_PART', 'random')}: nnz per worker max/mean "
+                  f"{max(nnz_k) / (sum(nnz_k) / K):.4f}", flush=True)
             for mode in [m for m in (("add", "average", "optimal") if K > 1 else ("average",))
                          if K == 1 or m in os.environ.get("DIST_MODES", "optimal,average,add")]:
                 solvers = [scd.Solver(sp, si, sv_, cfg.n_rows, nc, y, cfg.lam, "primal", seed=10 + k)
@@ -93,8 +100,9 @@ def main():
                 recs = run(solvers, mode, rounds, cfg.n_rows)
                 results[f"K={K} {mode}"] = recs
                 print(f"K={K} {mode:8s} gaps {' '.join('%.1e' % x['gap'] for x in recs)}", flush=True)
-                print(f"          gamma {' '.join('%.3f' % x['gamma'] for x in recs[:12])}  "
-                      f"worker epoch {np.mean([x['worker_ms_mean'] for x in recs]):.2f} ms", flush=True)
+                print(f"          gamma {' '.join('%.3f' % x['gamma'] for x in recs)}  "
+                      f"worker epoch mean {np.mean([x['worker_ms_mean'] for x in recs]):.2f} ms, "
+                      f"max {np.mean([x['worker_ms_max'] for x in recs]):.2f} ms", flush=True)
                 for s in solvers:
                     s.close()
             del shards
