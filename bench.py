@@ -477,7 +477,7 @@ def leg_c3(args, ctx):
 
 def leg_c4(args, ctx, d):
     """configs[3]: C3's matrix by feature.  N = 1: K = 1 epochs (roofline of the dominant bin, time to
-    1e-4).  N > 1: columns partitioned across the ranks (partition(seed 4), c15), optimal γ rounds."""
+    1e-4).  N > 1: columns partitioned across the ranks (balanced partition, c29), optimal γ rounds."""
     torch = ctx.torch
     import synth
     import paper_1702_07005_b200 as scd
@@ -490,7 +490,8 @@ def leg_c4(args, ctx, d):
     y = d["y"]
     world, rank = ctx.world, ctx.rank
     if world > 1:
-        owner = torch.from_numpy(scd.partition(4, M, world).astype(np.int64)).cuda()
+        # the library's structure-aware partition (stored-entry balanced, reading c29)
+        owner = torch.from_numpy(scd.partition_balanced(cp, 4, world).astype(np.int64)).cuda()
         cols = torch.nonzero(owner == rank).flatten()
         lens = (cp[1:] - cp[:-1])[cols]
         sp = torch.zeros(len(cols) + 1, dtype=torch.int64, device="cuda")
@@ -529,7 +530,8 @@ def leg_c4(args, ctx, d):
     del cp, ci, cv
     torch.cuda.empty_cache()
     return {"workload": "C4 (BASELINE configs[3]): C3's matrix by feature, primal TPA-SCD (CSC)"
-                        + (f", columns partitioned across {world} GPUs, optimal-gamma aggregation over NCCL each round"
+                        + (f", columns partitioned across {world} GPUs (stored-entry balanced), optimal-gamma "
+                           "aggregation over NCCL each round"
                            if world > 1 else ", K = 1"),
             "nnz_per_gpu": nnz, "columns_per_gpu": ncols, "ms_per_step": el_ms / steps,
             "nnz_per_s": nnz * world * steps / (el_ms / 1e3), "steps": steps, "roofline": roof,

@@ -17,6 +17,7 @@ import numpy as np
 import pytest
 
 import synth
+from envelope import check_band, envelope
 from oracle import ridge, solver
 
 pytestmark = pytest.mark.gpu
@@ -35,10 +36,10 @@ def c3p():
     d = synth.gen_host(synth.CONFIGS["C3"].with_rows(20_000))
     pr = solver.Problem.from_csr(d, lam=1e-3 * 350_000 / 20_000)
     _, _, hist = solver.solve(pr, "dual", E, seed=4)
-    return d, pr, hist
+    return d, pr, hist, envelope(pr, "dual", E)
 
 
-def _converge(d, pr, hist):
+def _converge(d, pr, hist, env):
     s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=4)
     info = s.info()
     gaps = []
@@ -55,8 +56,7 @@ def _converge(d, pr, hist):
     print("seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(Pg - Pstar) <= 1e-5 * abs(Pstar), (Pg, Pstar)
     assert gaps[-1] <= 1e-5
-    for t in (0, 1, 3):
-        assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
+    check_band(gaps, *env, label="c3 prefix")
     return info
 
 
@@ -103,7 +103,7 @@ def test_wild_variant_loses_updates(c3p):
     P:254): concurrent updates of the shared vector are lost, so w̄ drifts away from Aᵀα and the
     duality gap (from scratch, on α) stalls, while the atomic path keeps w̄ = Aᵀα within fp32 drift
     and reaches the optimum."""
-    d, pr, hist = c3p
+    d, pr, hist, _ = c3p
     A = pr.A()
     out = {}
     for wild in (False, True):
@@ -162,8 +162,7 @@ def test_hot_set_kernel_criteo_prefix(monkeypatch, implicit):
     print("seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert gaps[-1] <= 1e-5
-    for t in (0, 1, 3):
-        assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
+    check_band(gaps, *envelope(pr, "dual", 8), label="c5 prefix")
 
 
 def test_hot_set_kernel_ragged_short_rows(monkeypatch):
@@ -176,6 +175,7 @@ def test_hot_set_kernel_ragged_short_rows(monkeypatch):
     d = synth.gen_host(cfg)
     pr = solver.Problem.from_csr(d, lam=1.0)
     _, _, hist = solver.solve(pr, "dual", 6, seed=6)
+    env = envelope(pr, "dual", 6)
     A = pr.A()
     finals = {}
     for hot in ("4096", "0"):
@@ -190,8 +190,7 @@ def test_hot_set_kernel_ragged_short_rows(monkeypatch):
         x = s.get_model().astype(np.float64)
         s.close()
         print(hot, "gpu gaps", ["%.2e" % g for g in gaps])
-        for t in (0, 2):
-            assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (hot, t, gaps[t], hist[t]["gap"])
+        check_band(gaps, *env, label=f"ragged hot={hot}")
         finals[hot] = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
     print("seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(finals["4096"] - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
@@ -210,6 +209,7 @@ def test_tail_read_copy_ragged_two_bins(monkeypatch):
     d = synth.gen_host(cfg)
     pr = solver.Problem.from_csr(d, lam=1e-3 * 350_000 / 20_000)
     _, _, hist = solver.solve(pr, "dual", E, seed=7)
+    env = envelope(pr, "dual", E)
     s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=7)
     info = s.info()
     print("schedule", info)
@@ -234,8 +234,7 @@ def test_tail_read_copy_ragged_two_bins(monkeypatch):
     Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert gaps[-1] <= 1e-5
-    for t in (0, 1, 3):
-        assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
+    check_band(gaps, *env, label="ragged head")
 
 
 def test_schedule_rules_small_lambda():
@@ -245,6 +244,7 @@ def test_schedule_rules_small_lambda():
     d = synth.gen_host(synth.CONFIGS["C3"].with_rows(20_000))
     pr = solver.Problem.from_csr(d, lam=35.0 / 20_000)
     _, _, hist = solver.solve(pr, "dual", E, seed=4)
+    env = envelope(pr, "dual", E)
     s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=4)
     info = s.info()
     print("schedule", info)
@@ -270,5 +270,4 @@ def test_schedule_rules_small_lambda():
     Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert gaps[-1] <= 1e-5
-    for t in (0, 1, 3):
-        assert gaps[t] <= 10 * hist[t]["gap"] + 1e-9, (t, gaps[t], hist[t]["gap"])
+    check_band(gaps, *env, label="small lambda")
