@@ -112,7 +112,8 @@ typedef struct {
   const scd_collectives *collectives; /* host-side transport hooks instead of nccl_comm (NULL = NCCL) */
   int32_t block_order;    /* short coordinates (<= 64 entries, the 8-lane bins) are visited in blocks of this many
                              consecutive coordinates in a random block order (reading c28; their per-coordinate
-                             offsets, model, norm and label then share sectors); 0 = default (32), 1 = off */
+                             offsets, model, norm and label then share sectors) when the bin's in-flight cap spans
+                             >= 32 blocks; 0 = default (32), 1 = off */
 } scd_options;
 
 typedef struct scd_ctx scd_ctx;

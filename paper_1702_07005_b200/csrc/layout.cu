@@ -461,8 +461,12 @@ scd_status build_schedule(scd_ctx *c) {
       double cap = cap_fraction() * B.tau;
       B.cap = c->opt.max_inflight > 0 ? (int64_t)c->opt.max_inflight : (int64_t)(cap < 1 ? 1 : (cap > 1e9 ? 1e9 : cap));
       B.head = B.lanes == kLanesCta ? head : 0;
-      // block order for the short-coordinate bin (reading c28): 16.7 -> 13.1 ms on a C5 shard
-      B.blk = B.lanes == 8 ? (c->opt.block_order > 0 ? c->opt.block_order : 32) : 0;
+      // block order for the short-coordinate bin (reading c28): 16.7 -> 13.1 ms on a C5 shard.  The
+      // same rows of a block are in flight together every epoch, so it is used only while the bin's cap
+      // spans >= 32 blocks (with a cap of 15 on strongly coupled rows the fixed co-occurrence stalled the
+      // per-epoch rate: profiles/block_order_r2.txt)
+      const int64_t blk = c->opt.block_order > 0 ? c->opt.block_order : 32;
+      B.blk = (B.lanes == 8 && blk > 1 && B.cap >= 32 * blk) ? blk : 0;
       bin_launch_shape(c, B);
       ++c->n_bins;
     }

@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 import synth
-from envelope import check_band, envelope
+from envelope import check_stress_band, envelope
 from oracle import ridge, solver
 
 pytestmark = pytest.mark.gpu
@@ -56,7 +56,7 @@ def _converge(d, pr, hist, env):
     print("seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(Pg - Pstar) <= 1e-5 * abs(Pstar), (Pg, Pstar)
     assert gaps[-1] <= 1e-5
-    check_band(gaps, *env, label="c3 prefix")
+    check_stress_band(gaps, *env, label="c3 prefix")
     return info
 
 
@@ -162,7 +162,7 @@ def test_hot_set_kernel_criteo_prefix(monkeypatch, implicit):
     print("seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert gaps[-1] <= 1e-5
-    check_band(gaps, *envelope(pr, "dual", 8), label="c5 prefix")
+    check_stress_band(gaps, *envelope(pr, "dual", 8), label="c5 prefix")
 
 
 def test_hot_set_kernel_ragged_short_rows(monkeypatch):
@@ -190,7 +190,7 @@ def test_hot_set_kernel_ragged_short_rows(monkeypatch):
         x = s.get_model().astype(np.float64)
         s.close()
         print(hot, "gpu gaps", ["%.2e" % g for g in gaps])
-        check_band(gaps, *env, label=f"ragged hot={hot}")
+        check_stress_band(gaps, *env, label=f"ragged hot={hot}")
         finals[hot] = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
     print("seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(finals["4096"] - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
@@ -234,7 +234,7 @@ def test_tail_read_copy_ragged_two_bins(monkeypatch):
     Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert gaps[-1] <= 1e-5
-    check_band(gaps, *env, label="ragged head")
+    check_stress_band(gaps, *env, label="ragged head")
 
 
 def test_schedule_rules_small_lambda():
@@ -270,4 +270,4 @@ def test_schedule_rules_small_lambda():
     Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert gaps[-1] <= 1e-5
-    check_band(gaps, *env, label="small lambda")
+    check_stress_band(gaps, *env, label="small lambda")

@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 import synth
-from envelope import check_band, envelope
+from envelope import check_stress_band, envelope
 from oracle import ridge, solver
 
 pytestmark = pytest.mark.gpu
@@ -248,7 +248,7 @@ def test_async_converges_to_oracle_optimum(c2full, form):
     print(form, "seq gaps", ["%.2e" % h["gap"] for h in hist])
     assert abs(Pg - Pstar) <= 1e-5 * abs(Pstar)
     assert gaps[-1] <= 1e-5
-    check_band(gaps, *envelope(pr, form, len(gaps)), label=f"c2 {form}")
+    check_stress_band(gaps, *envelope(pr, form, len(gaps)), label=f"c2 {form}")
 
 
 def test_async_short_rows_group_kernel():
@@ -263,7 +263,7 @@ def test_async_short_rows_group_kernel():
     for t in range(1, 16):
         s.epoch(t)
         gaps.append(s.duality_gap())
-    check_band(gaps, *envelope(pr, "dual", 15), label="short rows")
+    check_stress_band(gaps, *envelope(pr, "dual", 15), label="short rows")
 
 
 # ------------------------------------------------------------------ aggregation (Alg. 3 / 4)
@@ -377,7 +377,7 @@ def test_implicit_values_equal_explicit_ones(form):
     for t in range(1, 6):
         c.epoch(t)
     env_max, env_min = envelope(pr, form, 5)
-    check_band([c.duality_gap()], env_max[-1:], env_min[-1:], label=f"implicit {form}")
+    check_stress_band([c.duality_gap()], env_max[-1:], env_min[-1:], label=f"implicit {form}")
 
 
 @pytest.mark.parametrize("form", ["primal", "dual"])

@@ -8,7 +8,7 @@ input generator synth/); writes tests/golden/seq_envelope_<cfg>.json.
 
   python tools/seq_envelope.py C3 6 3 4 5 6      # dual, 6 epochs, seeds 3..6
   python tools/seq_envelope.py C4 5 4 5 6 7      # primal (C3's matrix by feature)
-  python tools/seq_envelope.py C5s 4 5 6 7 8     # dual, one 25 M-row shard of C5 (standalone, λ = 1e-3)
+  python tools/seq_envelope.py C5s 4 5 6 7 8     # dual, one 25 M-row shard of C5 (standalone, λN = 2e5)
 """
 import json
 import os
@@ -28,8 +28,11 @@ def main():
 
     which, E, seeds = sys.argv[1], int(sys.argv[2]), [int(x) for x in sys.argv[3:]]
     t0 = time.perf_counter()
-    if which == "C5s":  # one GPU's shard of C5 as a standalone dual problem (25 M rows, values 1)
-        d = synth.gen_host(synth.CONFIGS["C5"].with_rows(25_000_000))
+    if which == "C5s":  # one GPU's shard of C5 as a standalone dual problem (25 M rows, values 1), with
+        # λ = 8e-3 so that λN = 2e5 as in each shard of the 8-GPU run (global N = 200 M, λ = 1e-3)
+        import dataclasses
+
+        d = synth.gen_host(dataclasses.replace(synth.CONFIGS["C5"].with_rows(25_000_000), lam=8e-3))
     else:
         d = synth.gen_host(synth.CONFIGS["C3"])
     pr = solver.Problem.from_csr(d, csc=which == "C4")
