@@ -222,21 +222,38 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------------------------
 class Ctx:
-    """Per-process state shared by the legs."""
+    """Per-process state shared by the legs.  BENCH_TRANSPORT=hooks (test mode only): the N ranks share
+    GPU 0 and the library's collectives go through the scd_collectives host hooks over gloo
+    (tests/hostcoll.py) — it exercises the N > 1 legs on a one-GPU box; its times are not results."""
 
     def __init__(self, rank, world, local):
         import torch
 
         self.torch = torch
         self.rank, self.world, self.local = rank, world, local
+        self.hooks = world > 1 and os.environ.get("BENCH_TRANSPORT") == "hooks"
         self.dist = None
+        self.hc = None
         if world > 1:
             import torch.distributed as dist
 
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if self.hooks:
+                dist.init_process_group("gloo")
+                sys.path.insert(0, os.path.join(ROOT, "tests"))
+                from hostcoll import HostCollectives
+
+                self.hc = HostCollectives()
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             self.dist = dist
         self.comm = None
         self.launches = 0
+
+    def comm_kw(self):
+        """The library's transport: an NCCL communicator, or (test mode) the host hooks."""
+        if self.hooks:
+            return dict(collectives=self.hc.struct)
+        return dict(nccl_comm=self.nccl())
 
     def barrier(self):
         if self.dist is not None:
@@ -245,7 +262,7 @@ class Ctx:
     def max_over_ranks(self, x: float) -> float:
         if self.dist is None:
             return x
-        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cpu" if self.hooks else "cuda")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -359,8 +376,8 @@ def leg_c3(args, ctx):
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     nnz = int(d["ptr"][-1].item())
-    comm = ctx.nccl()
-    kw = dict(seed=3 + rank, n_global=rows * world, rank=rank, world=world, nccl_comm=comm, max_inflight=args.max_inflight)
+    kw = dict(seed=3 + rank, n_global=rows * world, rank=rank, world=world, max_inflight=args.max_inflight,
+              **ctx.comm_kw())
     t_create = time.perf_counter()
     s = scd.Solver(d["ptr"], d["idx"], d["val"], rows, cfg.n_cols, d["y"], cfg.lam, "dual", profile=True, **kw)
     t_create = time.perf_counter() - t_create
@@ -505,7 +522,7 @@ def leg_c4(args, ctx, d):
     ncols = cp.numel() - 1
     nnz = int(cp[-1].item())
     s = scd.Solver(cp, ci, cv, N, ncols, y, cfg.lam, "primal", seed=4 + 10 * rank, profile=True, rank=rank,
-                   world=world, nccl_comm=ctx.nccl())
+                   world=world, **ctx.comm_kw())
     stream = torch.cuda.ExternalStream(s.stream_handle)
     info = s.info()
 
@@ -531,7 +548,7 @@ def leg_c4(args, ctx, d):
     torch.cuda.empty_cache()
     return {"workload": "C4 (BASELINE configs[3]): C3's matrix by feature, primal TPA-SCD (CSC)"
                         + (f", columns partitioned across {world} GPUs (stored-entry balanced), optimal-gamma "
-                           "aggregation over NCCL each round"
+                           "aggregation each round"
                            if world > 1 else ", K = 1"),
             "nnz_per_gpu": nnz, "columns_per_gpu": ncols, "ms_per_step": el_ms / steps,
             "nnz_per_s": nnz * world * steps / (el_ms / 1e3), "steps": steps, "roofline": roof,
@@ -557,7 +574,6 @@ def leg_c5(args, ctx):
     d["val"] = None
     torch.cuda.empty_cache()
     nnz = int(d["ptr"][-1].item())
-    comm = ctx.nccl()
     out = {"workload": f"C5 criteo-shaped (BASELINE configs[4]): {rows} rows x {cfg.n_cols} features per GPU, "
                        f"39 one-hot fields, implicit values (val = NULL), dual by example, global N = {n_global}",
            "nnz_per_gpu": nnz, "rows_per_gpu": rows, "n_global": n_global}
@@ -583,7 +599,7 @@ def leg_c5(args, ctx):
         s.close()
         return out
     s = scd.Solver(d["ptr"], d["idx"], None, rows, cfg.n_cols, d["y"], cfg.lam, "dual", seed=5 + rank,
-                   n_global=n_global, rank=rank, world=world, nccl_comm=comm)
+                   n_global=n_global, rank=rank, world=world, **ctx.comm_kw())
     stream = torch.cuda.ExternalStream(s.stream_handle)
     modes = {}
     for mode, max_rounds in (("optimal", 30), ("average", 15), ("add", 4)):
@@ -630,8 +646,9 @@ def main():
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_FEW_WARMUP"), "timing rules: warmup >= 3"
     import torch
 
-    torch.cuda.set_device(local)
-    if world > 1:
+    hooks = world > 1 and os.environ.get("BENCH_TRANSPORT") == "hooks"
+    torch.cuda.set_device(0 if hooks else local)
+    if world > 1 and not hooks:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # the driver can check the rank count / transport in the log
     ctx = Ctx(rank, world, local)
     rec, d = leg_c3(args, ctx)
@@ -702,6 +719,8 @@ def main():
             "clocks": rec["clocks"], "setup_s": rec["setup_s"],
             **subs,
         }
+        if hooks:
+            out["transport"] = "hooks (test mode: all ranks on GPU 0, collectives through host gloo; not a result)"
         print(json.dumps(out, default=float), flush=True)
     if ctx.comm:
         import paper_1702_07005_b200 as scd
