@@ -42,6 +42,7 @@ struct EpochArgs {
   int64_t roll_R;          // head kernel, rolling tail copy: every roll_R-th row refreshes one chunk (0 = off)
   int64_t head_P;          // head kernel, head copy in svr[0, H): every head_P-th row refreshes one chunk (0 = off)
   int64_t roll_lo, roll_hi;  // the tail range [roll_lo, roll_hi) kept in svr
+  int64_t nnz;               // stored entries (bound of the bulk copies of k_epoch_cluster_tma)
 };
 
 struct BinArgs {
@@ -949,6 +950,169 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
   }
 }
 
+// ----------------------------------------------------------------------------------------------
+// Heavy coordinates with their slices staged in shared memory by the bulk-copy engine (north_star
+// "(c)": TMA staging of long columns; C4's cluster bin: 10 385 columns of 16k-350k entries, 44% of
+// the entries).  Every CTA of the cluster owns one contiguous slice of the coordinate; its thread 0
+// issues one cp.async.bulk per array (idx, val) for the first CAP entries of the slice of the NEXT
+// coordinate into the other buffer of a double buffer (mbarrier with transaction count), so the
+// entries arrive while the current coordinate is computed; the dot and the scatter then read shared
+// memory (the rest of a slice longer than CAP streams from global as in k_epoch_cluster).  The next
+// coordinate is known one iteration early: CTA 0 takes its ticket while the current one is reduced
+// and publishes it with the delta, so a coordinate costs two cluster barriers (partials, delta) and
+// one CTA barrier instead of three cluster barriers.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+
+struct Slice {
+  int64_t beg, end;  // the CTA's entries [beg, end) of the coordinate
+  int64_t st;        // entries [beg, beg + st) are staged in shared memory, from offset off of the buffer
+  int off;
+};
+
+template <int CL, int CAP>
+__device__ __forceinline__ Slice cluster_slice(const EpochArgs &a, int64_t c, unsigned r) {
+  Slice q;
+  const int64_t b0 = __ldg(a.ptr + c), e0 = __ldg(a.ptr + c + 1);
+  const int64_t len = (e0 - b0 + CL - 1) / CL;
+  q.beg = min(e0, b0 + (int64_t)r * len);
+  q.end = min(e0, q.beg + len);
+  const int64_t a0 = q.beg & ~(int64_t)3;                        // 16-byte aligned copy start
+  int64_t a1 = (min(q.end, q.beg + (int64_t)CAP) + 3) & ~(int64_t)3;  // 16-byte aligned copy end
+  if (a1 > (a.nnz & ~(int64_t)3)) a1 = a.nnz & ~(int64_t)3;      // never read past the arrays
+  q.off = (int)(q.beg - a0);
+  const int64_t st = min(min(q.end, q.beg + (int64_t)CAP), a1) - q.beg;
+  q.st = st > 0 ? st : 0;
+  return q;
+}
+
+template <int FORM, int CL, int T, int CAP>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster_tma(EpochArgs a, BinArgs b) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int NW = T / 32;
+  constexpr int BUF = CAP + 4;  // staged entries + alignment slack
+  extern __shared__ float4 s_dyn[];
+  int32_t *s_idx = reinterpret_cast<int32_t *>(s_dyn);  // [2][BUF]
+  float *s_val = reinterpret_cast<float *>(s_idx + 2 * BUF);  // [2][BUF]
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ float s_red[NW];
+  __shared__ float s_part[CL];
+  __shared__ float s_delta;
+  __shared__ unsigned int s_tk[2];  // CTA 0: the tickets of the current and the next coordinate
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned r = cluster.block_rank();
+  float *part0 = cluster.map_shared_rank(s_part, 0);
+  float *delta0 = cluster.map_shared_rank(&s_delta, 0);
+  unsigned *tk0 = cluster.map_shared_rank(s_tk, 0);
+  const bool implicit = a.val == nullptr;
+  auto issue = [&](int buf, const Slice &q) {  // thread 0: bulk copies of the staged part of a slice
+    const int64_t a0 = q.beg - q.off;
+    const unsigned n = (unsigned)((q.off + q.st + 3) & ~3);
+    if (q.st <= 0) {
+      mbar_expect_tx(&s_bar[buf], 0);
+      return;
+    }
+    mbar_expect_tx(&s_bar[buf], n * 4u * (implicit ? 1u : 2u));
+    bulk_g2s(s_idx + buf * BUF, a.idx + a0, n * 4u, &s_bar[buf]);
+    if (!implicit) bulk_g2s(s_val + buf * BUF, a.val + a0, n * 4u, &s_bar[buf]);
+  };
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (r == 0) {
+      s_tk[0] = atomicAdd(b.counter, 1u);
+      s_tk[1] = atomicAdd(b.counter, 1u);
+    }
+  }
+  cluster.sync();
+  int64_t t_cur = b.lo + (int64_t)tk0[0], t_nxt = b.lo + (int64_t)tk0[1];
+  Slice cur{}, nxt{};
+  int64_t c_cur = -1, c_nxt = -1;
+  if (t_cur < b.hi) {
+    c_cur = bin_coord(b, t_cur);
+    cur = cluster_slice<CL, CAP>(a, c_cur, r);
+    if (tid == 0) issue(0, cur);
+  }
+  unsigned phase[2] = {0u, 0u};
+  int buf = 0;
+  for (;;) {
+    if (t_cur >= b.hi) break;  // cluster-uniform: every CTA read the same tickets
+    __syncthreads();           // the other buffer's previous coordinate is no longer read by this CTA
+    if (t_nxt < b.hi) {
+      c_nxt = bin_coord(b, t_nxt);
+      nxt = cluster_slice<CL, CAP>(a, c_nxt, r);
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(buf ^ 1, nxt);
+      }
+    }
+    mbar_wait(&s_bar[buf], phase[buf]);
+    phase[buf] ^= 1u;
+    const int32_t *bi = s_idx + buf * BUF + cur.off;
+    const float *bv = s_val + buf * BUF + cur.off;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int64_t k = tid; k < cur.st; k += T) acc = fmaf(ld_sv(a.svg + bi[k]), implicit ? 1.f : bv[k], acc);
+    acc += dot_strided<8>(a.svg, a.idx, a.val, cur.beg + cur.st + tid, cur.end, T);
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+      float sp = lane < NW ? s_red[lane] : 0.f;
+      sp = warp_sum(sp);
+      if (lane == 0) part0[r] = sp;
+    }
+    cluster.sync();  // partials in CTA 0
+    if (r == 0 && tid == 0) {
+      float sum = 0.f;
+      for (int i = 0; i < CL; ++i) sum += s_part[i];
+      const float xc = a.x[c_cur];
+      const float d = coord_delta<FORM>(sum, xc, __ldg(a.norm + c_cur), FORM == SCD_DUAL ? __ldg(a.y + c_cur) : 0.f,
+                                        a.lam, a.lamN);
+      if (!b.dry) a.x[c_cur] = xc + d;
+      s_delta = b.dry ? 0.f : d;
+      s_tk[0] = s_tk[1];  // every CTA read both tickets before the barrier above
+      s_tk[1] = t_nxt < b.hi ? atomicAdd(b.counter, 1u) : 0xFFFFFFFFu;
+    }
+    cluster.sync();  // delta and the next ticket published
+    const float d = scatter_scale<FORM>(*delta0);
+    const unsigned tk_new = tk0[1];
+    if (d != 0.f || b.dry) {
+#pragma unroll 8
+      for (int64_t k = tid; k < cur.st; k += T) red_add(a.sv + bi[k], (implicit ? 1.f : bv[k]) * d);
+      scatter_strided<8>(a.sv, a.idx, a.val, cur.beg + cur.st + tid, cur.end, T, d);
+    }
+    t_cur = t_nxt;
+    c_cur = c_nxt;
+    cur = nxt;
+    t_nxt = tk_new == 0xFFFFFFFFu ? b.hi : b.lo + (int64_t)tk_new;
+    buf ^= 1;
+  }
+  cluster.sync();  // nobody leaves while another CTA may still read CTA 0's shared memory
+}
+
 // kernel table ---------------------------------------------------------------------------------
 constexpr int kCtaT = kLanesCta, kCtaE = 16;
 constexpr int kGrpE8 = 8, kGrpE32 = 16;
@@ -978,9 +1142,21 @@ void *kernel_wild(int lanes) {
   }
 }
 
+constexpr int kClusterCap = 6144;  // staged entries per CTA slice (TMA cluster kernel): 2 x 48 KB double buffer
+
 template <int FORM, bool WILD>
-void *cluster_kernel() {
+void *cluster_kernel(bool tma) {
+  if (tma && !WILD) return (void *)k_epoch_cluster_tma<FORM, kClusterCtas, kClusterThreads, kClusterCap>;
   return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE, WILD>;
+}
+
+// the TMA cluster kernel needs 16-byte aligned idx / val arrays (bulk copies of aligned 16-byte units)
+bool cluster_tma_ok(const scd_ctx *c) {
+  return ((uintptr_t)c->idx % 16) == 0 && ((uintptr_t)c->val % 16) == 0 && !c->opt.wild;
+}
+
+size_t cluster_smem(const scd_ctx *c) {
+  return cluster_tma_ok(c) ? sizeof(int32_t) * 2 * 2 * (size_t)(kClusterCap + 4) : 0;
 }
 
 template <int FORM, int E, bool IMP>
@@ -1005,8 +1181,10 @@ void *bin_kernel(const scd_ctx *c, const Bin &b) {
   if (b.hot > 0 && b.lanes == 8 && !c->opt.wild)
     return c->form == SCD_PRIMAL ? hot_kernel<SCD_PRIMAL>(c, b) : hot_kernel<SCD_DUAL>(c, b);
   if (b.lanes == kLanesCluster) {
-    if (c->form == SCD_PRIMAL) return c->opt.wild ? cluster_kernel<SCD_PRIMAL, true>() : cluster_kernel<SCD_PRIMAL, false>();
-    return c->opt.wild ? cluster_kernel<SCD_DUAL, true>() : cluster_kernel<SCD_DUAL, false>();
+    const bool tma = cluster_tma_ok(c);
+    if (c->form == SCD_PRIMAL)
+      return c->opt.wild ? cluster_kernel<SCD_PRIMAL, true>(false) : cluster_kernel<SCD_PRIMAL, false>(tma);
+    return c->opt.wild ? cluster_kernel<SCD_DUAL, true>(false) : cluster_kernel<SCD_DUAL, false>(tma);
   }
   if (c->opt.wild) return c->form == SCD_PRIMAL ? kernel_wild<SCD_PRIMAL>(b.lanes) : kernel_wild<SCD_DUAL>(b.lanes);
   if (b.head > 0 && b.lanes == kLanesCta) {
@@ -1037,6 +1215,7 @@ EpochArgs make_args(scd_ctx *c) {
   a.roll_hi = c->tail_hi;
   a.lam = c->lam;
   a.lamN = c->lamN;
+  a.nnz = c->nnz;
   return a;
 }
 
@@ -1163,7 +1342,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
     if (block < 32) block = 32;
   }
-  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head : 0;
+  const size_t smem = b.head > 0 ? sizeof(float) * (size_t)b.head : (clus ? cluster_smem(c) : 0);
   if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
@@ -1213,7 +1392,8 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
     ha.P = (int)std::max<int64_t>(1, c->hot_copy);
     args = args_hot;
   }
-  const size_t smem = b.hot > 0 ? 8 * (size_t)b.hot : (b.head > 0 ? sizeof(float) * (size_t)b.head : 0);
+  const size_t smem = b.hot > 0 ? 8 * (size_t)b.hot
+                     : (b.head > 0 ? sizeof(float) * (size_t)b.head : (b.lanes == kLanesCluster ? cluster_smem(c) : 0));
   if (smem >= 48 * 1024) SCD_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(b.block), args, smem, s));
   return SCD_OK;
