@@ -186,6 +186,25 @@ def oracle_time_to_gap(d_dev, max_epochs: int = 3, target: float = 1e-4):
             "what": "full C3 (1.306e9 nnz), sequential fp64 SDCA (oracle.c), epochs to gap 1e-4"}
 
 
+def cpu_baseline_dist(K: int, rows: int = 400_000, rounds: int = 8):
+    """The oracle's Alg. 4 (optimal γ, dual by example) with K worker threads (SURVEY §8(d) oracle
+    timing protocol for K > 1): a bounded criteo-shaped sample (`rows` rows, field cardinalities
+    scaled by 1/100 so that each worker's copy of w̄ stays small), λN = 2e5 as in the C5 shards."""
+    import synth
+    from oracle import solver
+
+    cfg = synth.c5_scaled(rows, 1e-2)
+    d = synth.gen_host(cfg)
+    pr = solver.Problem.from_csr(d, lam=2e5 / rows, csc=False)
+    t0 = time.perf_counter()
+    solver.run_distributed(pr, "dual", K, "optimal", rounds, seed=5, seed_part=5, record=False, threads=K)
+    el = time.perf_counter() - t0
+    return {"value": pr.nnz * rounds / el, "unit": "nnz/s", "cores": K, "kind": "oracle",
+            "seconds_per_round": el / rounds, "host": host_info(),
+            "sample": f"Alg. 4 (optimal gamma) with {K} worker threads, {rounds} rounds, criteo-shaped rows [0,{rows}) "
+                      f"(fields scaled 1/100, {pr.nnz} nnz), lambda N = 2e5"}
+
+
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
@@ -693,6 +712,11 @@ def main():
         cpu = cpu_baseline(args.cpu_seconds)
         if oracle_ttg:
             cpu["time_to_gap_1e-4"] = oracle_ttg
+        if world > 1:
+            try:
+                cpu["distributed"] = cpu_baseline_dist(world)
+            except Exception as ex:
+                cpu["distributed"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     if rank == 0:
         cfg, info, rows, nnz, ttg = rec["cfg"], rec["info"], rec["rows"], rec["nnz"], rec["ttg"]

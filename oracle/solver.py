@@ -116,7 +116,7 @@ def solve(pr: Problem, form: str, epochs: int, seed: int, first_epoch: int = 1, 
 
 
 def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed: int, seed_part: int,
-                    first_epoch: int = 1, record: bool = True, parts: int = 1):
+                    first_epoch: int = 1, record: bool = True, parts: int = 1, threads: int = 1):
     """Distributed SCD, Alg. 3 (mode 'average', γ = 1/K) / 'add' (γ = 1) /
     Alg. 4 (mode 'optimal', γ from Eq. 7 corrected), simulated with K logical workers.
 
@@ -128,6 +128,8 @@ def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed
     parts > 1: sub-epoch rounds ("communicate shared vector updates more frequently"):
     round r runs part p = r mod parts of epoch t = first_epoch + r div parts, i.e. the positions
     [len·p/parts, len·(p+1)/parts) of each worker's epoch order, then aggregates.
+    threads > 1: the K local epochs of a round run in that many host threads (the epochs are C calls
+    that release the GIL; each worker owns its copies, so the result does not depend on it).
     Returns (model, shared, history) with history[i] = dict(epoch, gamma, P, D, gap)."""
     A = pr.A() if record else None
     n_coord = pr.M if form == "primal" else pr.N
@@ -147,7 +149,8 @@ def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed
         t, p = first_epoch + r // parts, r % parts
         dx = np.zeros_like(x0)
         ds = np.zeros_like(s0)
-        for k in range(K):
+
+        def local_epoch(k):
             xk = x0.copy()
             sk = s0.copy()
             nk = len(local[k])
@@ -156,6 +159,16 @@ def run_distributed(pr: Problem, form: str, K: int, mode: str, rounds: int, seed
                 primal_epoch(pr, xk, sk, order, nrm)
             else:
                 dual_epoch(pr, xk, sk, order, nrm, n_global=N)
+            return xk, sk
+
+        if threads > 1:
+            from concurrent.futures import ThreadPoolExecutor
+
+            with ThreadPoolExecutor(max_workers=threads) as ex:
+                results = list(ex.map(local_epoch, range(K)))
+        else:
+            results = [local_epoch(k) for k in range(K)]
+        for xk, sk in results:  # summed in worker order whatever the threads
             dx += xk - x0          # Δβ_k / Δα_k live on disjoint supports
             ds += sk - s0          # Σ_k Δw_k  (Alg. 3/4 "Aggregate updates")
         if mode == "add":

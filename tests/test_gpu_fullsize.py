@@ -109,7 +109,8 @@ def _side_by_side(form: str, band: float, envelope: str, cfg=None, seed: int = 3
             assert g <= band * env["envelope_max"][t], (t + 1, g, env["envelope_max"][t], band)
     # north_star tolerances at full size: gap <= 1e-5 and the objective within 1e-5 of the optimum
     assert gaps[gap_at - 1] <= 1e-5, gaps
-    assert Gstar <= 1e-8 and abs(Pg - Pstar) <= 1e-5 * abs(Pstar), (Pg, Pstar)
+    # P* is certified by the oracle's own gap (weak duality: P_orc - P* <= G_orc), 100x inside the tolerance
+    assert Gstar <= 1e-7 * abs(Pstar) and abs(Pg - Pstar) <= 1e-5 * abs(Pstar), (Pg, Pstar, Gstar)
     return A, x, sv, info
 
 
@@ -155,7 +156,7 @@ def test_c5_shard_full_size_against_oracle():
     # and the hot-set kernel's launch shape are those of the benchmarked shard (bench.py c5_shard)
     cfg = dataclasses.replace(synth.CONFIGS["C5"].with_rows(25_000_000), lam=8e-3)
     A, alpha, wbar, info = _side_by_side("dual", BAND, "C5s", cfg=cfg, seed=5, implicit=True, gpu_epochs=4,
-                                         oracle_epochs=6, gap_at=4)
+                                         oracle_epochs=7, gap_at=4)
     b = info["bins"][0]
     assert len(info["bins"]) == 1 and b["lanes"] == 8 and b["hot"] > 0, info
     v = A.T @ alpha

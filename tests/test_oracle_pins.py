@@ -355,6 +355,14 @@ def test_adaptive_never_worse_than_average(form):
 
 
 @pytest.mark.slow
+def test_distributed_threads_do_not_change_the_result():
+    pr = _rand_prob(120, 60, 0.2, 77, 0.01)
+    for form in ("primal", "dual"):
+        a = solver.run_distributed(pr, form, 4, "optimal", 3, seed=1, seed_part=2)
+        b = solver.run_distributed(pr, form, 4, "optimal", 3, seed=1, seed_part=2, threads=4)
+        assert np.array_equal(a[0], b[0]) and [h["gamma"] for h in a[2]] == [h["gamma"] for h in b[2]]
+
+
 def test_distributed_slowdown_shape():
     """Fig. 3 shape ("approximately linear slow-down"): with averaging, epochs to a
     fixed gap are nondecreasing in K; adaptive aggregation (Alg. 4) at K = 8 needs fewer epochs
