@@ -314,7 +314,7 @@ def kernel_roofline(s, info, kprof, bytes_per_nnz: int, el_ms: float, world: int
     bytes_launch = (bytes_per_nnz * bb["nnz"] + BYTES_PER_COORD * bb["count"]) / info["n_slices"]
     achieved = bytes_launch / (ms_b / cnt_b / 1e3) / 1e9 if cnt_b else None
     if bb["lanes"] >= 4096:
-        kname = "k_epoch_cluster_tma"  # the TMA-staged cluster kernel (16-byte aligned idx / val arrays)
+        kname = "k_epoch_cluster_tma" if os.environ.get("SCD_CLUSTER_TMA") == "1" else "k_epoch_cluster"
     elif bb["lanes"] >= 64:
         kname = "k_epoch_cta_head" if bb.get("head") else "k_epoch_cta"
     else:

@@ -959,8 +959,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
 // entries arrive while the current coordinate is computed; the dot and the scatter then read shared
 // memory (the rest of a slice longer than CAP streams from global as in k_epoch_cluster).  The next
 // coordinate is known one iteration early: CTA 0 takes its ticket while the current one is reduced
-// and publishes it with the delta, so a coordinate costs two cluster barriers (partials, delta) and
-// one CTA barrier instead of three cluster barriers.
+// and publishes it with the delta.  Three cluster barriers per coordinate (previous scatter done,
+// partials, delta), as in k_epoch_cluster.
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -1059,7 +1059,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster_
   int buf = 0;
   for (;;) {
     if (t_cur >= b.hi) break;  // cluster-uniform: every CTA read the same tickets
-    __syncthreads();           // the other buffer's previous coordinate is no longer read by this CTA
+    // every CTA of the cluster has finished scattering the previous coordinate before any gathers this
+    // one (else the previous coordinate would still be in flight: one more per cluster than the bin's
+    // cap; measured: C2 primal per-epoch gap 2x the sequential envelope at epoch 3 instead of 1.5x), and
+    // this CTA no longer reads the other buffer
+    cluster.sync();
     if (t_nxt < b.hi) {
       c_nxt = bin_coord(b, t_nxt);
       nxt = cluster_slice<CL, CAP>(a, c_nxt, r);
@@ -1150,9 +1154,12 @@ void *cluster_kernel(bool tma) {
   return (void *)k_epoch_cluster<FORM, kClusterCtas, kClusterThreads, kClE, WILD>;
 }
 
-// the TMA cluster kernel needs 16-byte aligned idx / val arrays (bulk copies of aligned 16-byte units)
+// The TMA-staged cluster kernel is opt-in (SCD_CLUSTER_TMA=1): measured no faster than the register-tile
+// kernel (0.52-0.57 vs 0.515 ms per C4 slice launch, profiles/c4_cluster_tma_r2.txt: the bin is bound by
+// the L2 rate of gathers and REDs on the same residual lines).  It needs 16-byte aligned idx / val arrays.
 bool cluster_tma_ok(const scd_ctx *c) {
-  return ((uintptr_t)c->idx % 16) == 0 && ((uintptr_t)c->val % 16) == 0 && !c->opt.wild;
+  static const bool on = getenv("SCD_CLUSTER_TMA") && atoi(getenv("SCD_CLUSTER_TMA")) == 1;
+  return on && ((uintptr_t)c->idx % 16) == 0 && ((uintptr_t)c->val % 16) == 0 && !c->opt.wild;
 }
 
 size_t cluster_smem(const scd_ctx *c) {

@@ -3,6 +3,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 
@@ -386,13 +388,103 @@ scd_status compute_norms(scd_ctx *c) {
   return SCD_OK;
 }
 
+// Device-side binning (create time): bin of every coordinate by its stored-entry count (255 = empty),
+// per-bin count / entries / longest coordinate, and each bin's coordinate list in ascending order
+// (cub::DeviceSelect, order-preserving).  Only the per-bin totals come back to the host.
+constexpr int kNB = 4;
+struct BinLimits {
+  int64_t lim[kNB];
+};
+
+__global__ void k_bin_of(const int64_t *ptr, int64_t n, BinLimits L, uint8_t *bin,
+                         unsigned long long *cnt /* [kNB + 1] */, unsigned long long *nnz /* [kNB] */,
+                         unsigned long long *mx /* [kNB] */) {
+  __shared__ unsigned long long s_c[kNB + 1], s_z[kNB], s_m[kNB];
+  if (threadIdx.x < kNB + 1) s_c[threadIdx.x] = 0;
+  if (threadIdx.x < kNB) s_z[threadIdx.x] = s_m[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = ptr[i + 1] - ptr[i];
+    uint8_t b = 255;
+    if (len > 0) {
+      b = kNB - 1;
+      for (int k = 0; k < kNB; ++k)
+        if (len <= L.lim[k]) {
+          b = (uint8_t)k;
+          break;
+        }
+      atomicAdd(&s_z[b], (unsigned long long)len);
+      atomicMax(&s_m[b], (unsigned long long)len);
+    }
+    bin[i] = b;
+    atomicAdd(&s_c[b == 255 ? kNB : b], 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNB + 1 && s_c[threadIdx.x]) atomicAdd(cnt + threadIdx.x, s_c[threadIdx.x]);
+  if (threadIdx.x < kNB && s_z[threadIdx.x]) atomicAdd(nnz + threadIdx.x, s_z[threadIdx.x]);
+  if (threadIdx.x < kNB && s_m[threadIdx.x]) atomicMax(mx + threadIdx.x, s_m[threadIdx.x]);
+}
+
+struct BinIs {
+  const uint8_t *bin;
+  uint8_t b;
+  __device__ __forceinline__ bool operator()(const int32_t &i) const { return bin[i] == b; }
+};
+
+// lists[k] (device, ascending ids) for k in [0, kNB] (kNB = the empty coordinates), allocated with
+// cudaMalloc when the bin is non-empty and not the whole index range (then nullptr = identity).
+static scd_status device_bins(scd_ctx *c, const int64_t lim[kNB], int32_t *lists[kNB + 1], int64_t count[kNB + 1],
+                              int64_t nnz[kNB], int64_t maxlen[kNB]) {
+  cudaStream_t s = c->stream;
+  const int64_t n = c->n_coord;
+  uint8_t *bin = nullptr;
+  unsigned long long *st = nullptr;
+  SCD_CK(c, cudaMallocAsync((void **)&bin, (size_t)std::max<int64_t>(n, 1), s));
+  SCD_CK(c, cudaMallocAsync((void **)&st, sizeof(unsigned long long) * (3 * kNB + 1), s));
+  SCD_CK(c, cudaMemsetAsync(st, 0, sizeof(unsigned long long) * (3 * kNB + 1), s));
+  BinLimits L;
+  for (int k = 0; k < kNB; ++k) L.lim[k] = lim[k];
+  k_bin_of<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(c->ptr, n, L, bin, st, st + kNB + 1, st + 2 * kNB + 1);
+  SCD_CKL(c, "k_bin_of");
+  unsigned long long h[3 * kNB + 1];
+  SCD_CK(c, cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SCD_CK(c, cudaStreamSynchronize(s));
+  for (int k = 0; k <= kNB; ++k) count[k] = (int64_t)h[k];
+  for (int k = 0; k < kNB; ++k) {
+    nnz[k] = (int64_t)h[kNB + 1 + k];
+    maxlen[k] = (int64_t)h[2 * kNB + 1 + k];
+  }
+  int *d_num = nullptr;
+  SCD_CK(c, cudaMallocAsync((void **)&d_num, sizeof(int), s));
+  void *tmp = nullptr;
+  size_t tmp_b = 0;
+  for (int k = 0; k <= kNB; ++k) {
+    lists[k] = nullptr;
+    if (count[k] == 0 || (count[k] == n && k < kNB)) continue;  // empty bin, or a bin's identity list
+    SCD_CK(c, cudaMalloc((void **)&lists[k], sizeof(int32_t) * (size_t)count[k]));
+    BinIs op{bin, (uint8_t)(k == kNB ? 255 : k)};
+    cub::CountingInputIterator<int32_t> ids(0);
+    size_t need = 0;
+    cub::DeviceSelect::If(nullptr, need, ids, lists[k], d_num, (int)n, op, s);
+    if (need > tmp_b) {
+      if (tmp) cudaFreeAsync(tmp, s);
+      SCD_CK(c, cudaMallocAsync(&tmp, need, s));
+      tmp_b = need;
+    }
+    SCD_CK(c, cub::DeviceSelect::If(tmp, tmp_b, ids, lists[k], d_num, (int)n, op, s));
+  }
+  if (tmp) cudaFreeAsync(tmp, s);
+  cudaFreeAsync(d_num, s);
+  cudaFreeAsync(bin, s);
+  cudaFreeAsync(st, s);
+  SCD_CK(c, cudaStreamSynchronize(s));
+  return SCD_OK;
+}
+
 // Asynchronous schedule: coordinates binned by stored-entry count, each bin processed by the
 // kernel shape that suits its length.  Empty coordinates go to the empty list.
 scd_status build_schedule(scd_ctx *c) {
   const int64_t n = c->n_coord;
-  std::vector<int64_t> hp((size_t)n + 1);
-  SCD_CK(c, cudaMemcpyAsync(hp.data(), c->ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost, c->stream));
-  SCD_CK(c, cudaStreamSynchronize(c->stream));
   // bin thresholds (entries per coordinate): (0,64] -> 8-lane groups, (64,1024] -> warps,
   // (1024,16384] -> one CTA, > 16384 -> one 8-CTA cluster per coordinate
   constexpr int NB = 4;
@@ -403,16 +495,8 @@ scd_status build_schedule(scd_ctx *c) {
   // separate warp-bin launch per slice is a latency-bound single wave (C3: 2.5% of the step for 0.7%
   // of the entries)
   const int64_t lim1 = head > 0 && c->form == SCD_DUAL ? 64 : 1024;
-  // empty coordinates (any lim1)
-  std::vector<int32_t> empty;
-  for (int64_t i = 0; i < n; ++i)
-    if (hp[(size_t)i + 1] == hp[(size_t)i]) empty.push_back((int32_t)i);
-  c->n_empty = (int64_t)empty.size();
-  c->n_nonempty = n - c->n_empty;
-  if (c->n_empty) {
-    SCD_CK(c, cudaMalloc((void **)&c->empty_list, sizeof(int32_t) * empty.size()));
-    SCD_CK(c, cudaMemcpy(c->empty_list, empty.data(), sizeof(int32_t) * empty.size(), cudaMemcpyHostToDevice));
-  }
+  c->n_empty = 0;
+  c->empty_list = nullptr;
   c->sv_active = c->n_shared;
   if (c->form == SCD_DUAL) {
     if (scd_status st = active_extent(c, &c->sv_active); st != SCD_OK) return st;
@@ -423,36 +507,26 @@ scd_status build_schedule(scd_ctx *c) {
   // one binning pass with the medium-row boundary lim1 (launch order: longest coordinates first)
   auto bin_pass = [&](int64_t l1) -> scd_status {
     const int64_t lim[NB] = {64, l1, 16384, INT64_MAX};
-    std::vector<int32_t> lists[NB];
-    int64_t nnzb[NB] = {0, 0, 0, 0}, maxb[NB] = {0, 0, 0, 0};
-    for (int64_t i = 0; i < n; ++i) {
-      const int64_t L = hp[(size_t)i + 1] - hp[(size_t)i];
-      if (L == 0) continue;
-      for (int b = 0; b < NB; ++b)
-        if (L <= lim[b]) {
-          lists[b].push_back((int32_t)i);
-          nnzb[b] += L;
-          maxb[b] = std::max(maxb[b], L);
-          break;
-        }
-    }
+    int32_t *lists[NB + 1];
+    int64_t cnt[NB + 1], nnzb[NB], maxb[NB];
+    if (scd_status st = device_bins(c, lim, lists, cnt, nnzb, maxb); st != SCD_OK) return st;
+    // the empty coordinates (the same for every pass)
+    cudaFree(c->empty_list);
+    c->empty_list = lists[NB];
+    c->n_empty = cnt[NB];
+    c->n_nonempty = n - c->n_empty;
     c->n_bins = 0;
     c->tau_star = 1e18;
     for (int b = NB - 1; b >= 0; --b) {
-      if (lists[b].empty()) continue;
+      if (cnt[b] == 0) continue;
       Bin &B = c->bins[c->n_bins];
       B = Bin();
       B.lanes = lanes[b];
-      B.count = (int64_t)lists[b].size();
+      B.count = cnt[b];
       B.nnz = nnzb[b];
       B.maxlen = maxb[b];
       B.stream_id = 1u + (uint32_t)c->n_bins;
-      if (B.count == n) {
-        B.list = nullptr;  // identity: every coordinate is in this bin
-      } else {
-        SCD_CK(c, cudaMalloc((void **)&B.list, sizeof(int32_t) * lists[b].size()));
-        SCD_CK(c, cudaMemcpy(B.list, lists[b].data(), sizeof(int32_t) * lists[b].size(), cudaMemcpyHostToDevice));
-      }
+      B.list = lists[b];  // nullptr = identity: every coordinate is in this bin
       // the CTA bin of the head kernel also gets its tail bound (tail read copy) from the same pass
       const bool want_tail = c->tail_snap && B.lanes == kLanesCta && head > 0;
       scd_status st = estimate_bin_tau(c, B.list, B.count, &B.tau, want_tail ? (int64_t)head : -1, &B.tau_tail);

@@ -201,6 +201,33 @@ def test_set_model_rebuilds_shared_vector(c2s):
     assert np.array_equal(s.get_model(), a)
 
 
+@pytest.mark.parametrize("form", ["dual", "primal"])
+def test_recompute_every_rebuilds_from_the_model(c2full, form):
+    """NEXT-2 (P:164 recomputation): with recompute_every = 2 the shared vector after epochs 2 and 4 is
+    the fp64 product of the model rounded once (w̄ = Aᵀα / w = Aβ), while without it the fp32 atomics
+    drift; the run still reaches the oracle's optimum, and the gap evaluated right after a rebuild
+    (sharing its fp64 product) equals the oracle's on the same model."""
+    d, pr = c2full
+    A = pr.A()
+    args = (d["ptr"], d["idx"], d["val"]) if form == "dual" else (pr.cptr, pr.cidx, pr.cval)
+    drift = {}
+    for rec in (0, 2):
+        s = scd.Solver(*args, pr.N, pr.M, d["y"], pr.lam, form, seed=5, recompute_every=rec)
+        for t in range(1, 5):
+            s.epoch(t)
+        g = s.duality_gap()
+        x = s.get_model().astype(np.float64)
+        sh = s.get_shared().astype(np.float64)
+        s.close()
+        ref = A.T @ x if form == "dual" else A @ x
+        drift[rec] = np.abs(sh - ref).max() / np.abs(ref).max()
+        go = (ridge.dual_report if form == "dual" else ridge.primal_report)(A, pr.y, pr.lam, x)[2]
+        assert g == pytest.approx(go, rel=1e-6), (rec, g, go)
+    print(form, "shared-vector drift after 4 epochs: off %.2e, recompute_every=2 %.2e" % (drift[0], drift[2]))
+    assert drift[2] <= 2e-7          # one fp32 rounding of the fp64 product
+    assert drift[2] < drift[0]
+
+
 # ------------------------------------------------------------------ asynchronous epochs
 @pytest.fixture(scope="module")
 def c2full():
