@@ -335,6 +335,31 @@ def test_logical_k_aggregation_matches_oracle(form, mode):
 
 
 @pytest.mark.parametrize("form", ["primal", "dual"])
+def test_logical_k4_ten_rounds_optimal(form):
+    """Ten optimal-γ rounds with K = 4 logical workers (the verdict's stability check at the level of
+    parity): every round's γ (base-point scalars, reading c30) and the final models against the
+    Alg. 4 simulator, and the gap from the fused group evaluation against the oracle's."""
+    d = synth.gen_host(synth.CONFIGS["C2"].with_rows(1500))
+    pr = solver.Problem.from_csr(d)
+    K, seed, sp_, rounds = 4, 10, 3, 10
+    xo, so, hist = solver.run_distributed(pr, form, K, "optimal", rounds, seed=seed, seed_part=sp_)
+    solvers = [scd.Solver(p, i, v, nr, nc, y, pr.lam, form, seed=seed + k, deterministic=True, n_global=pr.N)
+               for k, (p, i, v, nr, nc, y) in enumerate(_shards(d, pr, form, K, sp_))]
+    for t in range(1, rounds + 1):
+        for s in solvers:
+            s.epoch(t)
+        g = scd.aggregate_group(solvers, "optimal")
+        assert g == pytest.approx(hist[t - 1]["gamma"], rel=1e-4, abs=1e-7), (t, g, hist[t - 1]["gamma"])
+    P, D, gap = scd.evaluate_group(solvers)
+    assert gap == pytest.approx(hist[-1]["gap"], rel=1e-3, abs=1e-12)
+    owner = oracle.partition(sp_, pr.M if form == "primal" else pr.N, K)
+    x = np.zeros(len(owner))
+    for k, s in enumerate(solvers):
+        x[owner == k] = s.get_model()
+    assert _rel(x, xo) <= 1e-4
+
+
+@pytest.mark.parametrize("form", ["primal", "dual"])
 def test_nccl_single_rank_aggregate_and_gap(c2s, form):
     """The NCCL code path (all-reduce of Δ and the scalars, all-reduce inside the gap) with a
     1-rank communicator must equal the communicator-free result."""
