@@ -55,7 +55,10 @@ void free_ctx(scd_ctx *c) {
   cudaFree(c->svr);
   cudaFree(c->norm);
   cudaFree(c->empty_list);
-  for (int i = 0; i < kMaxBins; ++i) cudaFree(c->bins[i].list);
+  for (int i = 0; i < kMaxBins; ++i) {
+    cudaFree(c->bins[i].list);
+    cudaFree(c->bins[i].bperm);
+  }
   cudaFree(c->counters);
   cudaFree(c->hot_idx);
   cudaFree(c->hot_ids);

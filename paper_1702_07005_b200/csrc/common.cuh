@@ -99,6 +99,8 @@ struct Bin {
   int grid = 0, block = 0;
   uint32_t stream_id = 0;    // permutation stream = 1 + bin index
   int64_t blk = 0;           // > 1: the epoch visits blocks of blk consecutive coordinates (reading c28)
+  int blk_shift = 0;         // log2(blk)
+  int32_t *bperm = nullptr;  // device [count / blk]: the epoch's block permutation (k_block_perm)
   double ms = 0.0;           // profiling accumulator
   int64_t prof_launches = 0;
 };

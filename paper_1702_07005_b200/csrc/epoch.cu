@@ -49,6 +49,8 @@ struct BinArgs {
   const int32_t *list;  // coordinate ids of the bin (ascending); nullptr = identity
   int64_t lo, hi;       // this launch processes permutation positions [lo, hi) of the bin
   int64_t blk;          // > 1: block order (reading c28): perm permutes the count / blk full blocks
+  int blk_shift;        // log2(blk) (blk is a power of two)
+  const int32_t *bperm; // block order: the epoch's block permutation materialised (nullptr: evaluate perm)
   int zero;             // 0 at run time (ticket_async)
   unsigned int *counter;
   Perm perm;
@@ -150,8 +152,10 @@ __device__ __forceinline__ unsigned ticket_async(const struct BinArgs &b, unsign
 __device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
   uint64_t j;
   if (b.blk > 1) {
-    const uint64_t blk = (uint64_t)b.blk, tb = t / blk;
-    j = tb < b.perm.n ? perm_apply(b.perm, tb) * blk + (t - tb * blk) : t;
+    const uint64_t tb = t >> b.blk_shift;
+    j = tb < b.perm.n ? (((b.bperm ? (uint64_t)__ldg(b.bperm + tb) : perm_apply(b.perm, tb)) << b.blk_shift) |
+                         (t & (uint64_t)(b.blk - 1)))
+                      : t;
   } else {
     j = perm_apply(b.perm, t);
   }
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(T, 1) k_epoch_group_hot(EpochArgs a, BinArgs b
     if (lane == 0) tk_pf = ticket_async(b, (unsigned)CPW);
     if (HC && !b.dry) {
       const int64_t tk = (b.lo + (int64_t)t0) / CPW;
-      if (tk % h.P == 0) {
+      if ((tk & (int64_t)(h.P - 1)) == 0) {  // h.P is a power of two
         const int nch = (h.K + 31) / 32;
         const int sl = (int)((tk / h.P) % nch) * 32 + lane;
         if (sl < h.K) h.hc[sl] = __ldcg(a.sv + s_hid[sl]);
@@ -855,6 +859,13 @@ __global__ void k_empty_fix(EpochArgs a, const int32_t *list, int64_t n) {
 __global__ void k_perm_export(Perm p, int64_t n, int64_t *out) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
     out[j] = (int64_t)perm_apply(p, (uint64_t)j);
+}
+
+// the epoch's block permutation of a block-ordered bin, materialised once per bin and epoch (the Feistel
+// evaluation was ~15% of the hot-set kernel's instructions: profiles/c5_shape_r2.txt)
+__global__ void k_block_perm(Perm p, int64_t nf, int32_t *out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)perm_apply(p, (uint64_t)i);
 }
 
 // the epoch order of a bin in block order (reading c28), through bin_coord itself (identity list)
@@ -1313,7 +1324,9 @@ void hot_launch_shape(scd_ctx *c, Bin &b) {
       c->hot_hc = nullptr;
       return;
     }
-    c->hot_copy = P;
+    int64_t p2 = 1;  // a power of two (the take() test is a mask): the copy's age only shrinks
+    while (p2 * 2 <= P) p2 *= 2;
+    c->hot_copy = p2;
     b.flush = (int)f;
   }
   // the early hot gathers read the copy: without it the kernel reads the hot values in their turn
@@ -1451,8 +1464,18 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
       if (ba.hi <= ba.lo) continue;
       ba.counter = c->counters + sl * kMaxBins + i;
       ba.blk = b.blk;
+      ba.blk_shift = b.blk_shift;
+      ba.bperm = nullptr;
       ba.zero = 0;
       ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.blk > 1 ? b.count / b.blk : b.count);
+      if (b.blk > 1 && b.bperm && ba.perm.n > 0) {
+        if (sl == 0) {  // once per epoch and bin (every slice uses the same permutation)
+          k_block_perm<<<grid_for((int64_t)ba.perm.n, 256), 256, 0, s>>>(ba.perm, (int64_t)ba.perm.n, b.bperm);
+          SCD_CKL(c, "k_block_perm launch");
+          ++c->launches;
+        }
+        ba.bperm = b.bperm;
+      }
       ba.dry = 0;
       const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;  // coordinates per CTA (or cluster) per round
       const int unit = b.lanes == kLanesCluster ? b.cl : 1;
@@ -1528,6 +1551,8 @@ scd_status tune_shared_layout(scd_ctx *c) {
     ba.lo = 0;
     ba.hi = probe;
     ba.blk = b.blk;
+    ba.blk_shift = b.blk_shift;
+    ba.bperm = nullptr;  // the probe's permutation differs from the epochs': evaluated inline
     ba.zero = 0;
     ba.perm = make_perm(c->opt.seed ^ 0x5052424Full, 0xFFFFFFFEu, b.stream_id, b.blk > 1 ? b.count / b.blk : b.count);
     ba.dry = 1;
@@ -1588,6 +1613,9 @@ scd_status launch_block_order_export(uint64_t seed, uint32_t epoch, uint32_t str
   b.lo = 0;
   b.hi = n;
   b.blk = blk;
+  b.blk_shift = 0;
+  while ((1ll << (b.blk_shift + 1)) <= blk) ++b.blk_shift;
+  b.bperm = nullptr;
   b.perm = make_perm(seed, epoch, stream, blk > 1 ? n / blk : n);
   k_block_order_export<<<grid_for(n, 256), 256, 0, s>>>(b, n, d_out);
   return cudaGetLastError() == cudaSuccess ? SCD_OK : SCD_E_CUDA;

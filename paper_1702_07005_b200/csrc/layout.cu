@@ -539,8 +539,13 @@ scd_status build_schedule(scd_ctx *c) {
       // same rows of a block are in flight together every epoch, so it is used only while the bin's cap
       // spans >= 32 blocks (with a cap of 15 on strongly coupled rows the fixed co-occurrence stalled the
       // per-epoch rate: profiles/block_order_r2.txt)
-      const int64_t blk = c->opt.block_order > 0 ? c->opt.block_order : 32;
+      int64_t blk = 1;  // a power of two (the epoch order uses shifts and masks)
+      while (blk * 2 <= (c->opt.block_order > 0 ? c->opt.block_order : 32)) blk *= 2;
       B.blk = (B.lanes == 8 && blk > 1 && B.cap >= 32 * blk) ? blk : 0;
+      B.blk_shift = 0;
+      while ((1ll << (B.blk_shift + 1)) <= B.blk) ++B.blk_shift;
+      if (B.blk > 1 && B.count / B.blk > 0)
+        SCD_CK(c, cudaMalloc((void **)&B.bperm, sizeof(int32_t) * (size_t)(B.count / B.blk)));
       bin_launch_shape(c, B);
       ++c->n_bins;
     }
@@ -555,6 +560,7 @@ scd_status build_schedule(scd_ctx *c) {
     if (!head_used) {
       for (int i = 0; i < c->n_bins; ++i) {
         cudaFree(c->bins[i].list);
+        cudaFree(c->bins[i].bperm);
         c->bins[i] = Bin();
       }
       if (scd_status st = bin_pass(1024); st != SCD_OK) return st;
