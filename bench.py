@@ -316,7 +316,7 @@ def kernel_roofline(s, info, kprof, bytes_per_nnz: int, el_ms: float, world: int
     if bb["lanes"] >= 4096:
         kname = "k_epoch_cluster_tma" if os.environ.get("SCD_CLUSTER_TMA") == "1" else "k_epoch_cluster"
     elif bb["lanes"] >= 64:
-        kname = "k_epoch_cta_head" if bb.get("head") else "k_epoch_cta"
+        kname = ("k_epoch_sm_tma" if info.get("sm_head") else "k_epoch_cta_head") if bb.get("head") else "k_epoch_cta"
     else:
         kname = "k_epoch_group_hot" if bb.get("hot") else ("k_epoch_group_comb" if bb["lanes"] == 8 else "k_epoch_group")
     traffic, dram_bytes = None, None
@@ -424,6 +424,10 @@ def leg_c3(args, ctx):
     if roof and roof["kernel"] == "k_epoch_cta_head" and info.get("tail_roll"):
         roof["kernel"] += (f" (head {info['bins'][roof['bin']]['head']} floats combined, flush every "
                            f"{info['bins'][roof['bin']]['flush']}, head/tail gathers from the rolling read copies)")
+    if roof and roof["kernel"] == "k_epoch_sm_tma":
+        roof["kernel"] += (f" ({info['sm_head']} row groups per SM sharing the head snapshot and pending updates of "
+                           f"w̄[0, {info['bins'][roof['bin']]['head']}), rows bulk-copied to shared memory in "
+                           f"{info['sm_chunk']}-entry chunks, tail gathers from the rolling read copy)")
 
     # access-pattern ceiling on this box: the same gathers + REDs over the same matrix with no
     # algorithmic dependency (tools/pattern_bench.cu), against a scratch vector

@@ -235,6 +235,13 @@ typedef struct {
   double hot_tail_tau;    /* staleness bound of the hot bin's coupling through its non-hot entries; the early
                              gather is used only while 2 x rows in flight <= hot_tail_tau / 2 */
   int32_t hot_hp;         /* 1: the hot values of the next batch are also gathered one step early (from the copy) */
+  int32_t sm_head;        /* > 0: the head bin runs the SM-shared head kernel with this many row groups per SM
+                             (one CTA per SM sharing a snapshot of w̄[0, bin_head) and its pending updates;
+                             rows staged in shared memory by bulk copies); 0 = off */
+  int32_t sm_chunk;       /* SM-shared head kernel: entries per bulk-copied chunk of a row */
+  int32_t sm_ch;          /* SM-shared head kernel: head chunks (1024 floats) flushed and re-read per flushing row */
+  int32_t sm_rh;          /* SM-shared head kernel: rows per flushing row (an SM's head chunk rotates every
+                             bin_head / 1024 / sm_ch * sm_rh of its rows) */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

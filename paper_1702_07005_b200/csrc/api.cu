@@ -529,6 +529,14 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->hot_tp = c->hot_tp ? 1 : 0;
   info->hot_hp = (c->hot_hp && c->hot_copy > 0 && c->hot_tp) ? 1 : 0;
   info->hot_tail_tau = c->hot_tail_tau;
+  info->sm_head = info->sm_chunk = info->sm_ch = info->sm_rh = 0;
+  for (int i = 0; i < c->n_bins && i < 4; ++i)
+    if (c->bins[i].sm) {
+      info->sm_head = c->bins[i].sm;
+      info->sm_chunk = sm_chunk_entries();
+      info->sm_ch = c->bins[i].sm_ch;
+      info->sm_rh = c->bins[i].sm_rh;
+    }
   info->inflight_cap = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i) {
     info->bin_cap[i] = c->bins[i].cap;

@@ -91,6 +91,9 @@ struct Bin {
   int flush = 0;             // head kernel: coordinates per CTA between flushes of the pending head
   int cl = kClusterCtas;     // cluster bin: CTAs per cluster (one coordinate per cluster)
   int hot = 0;               // 8-lane bin: > 0 = hot-set kernel with this many hot slots (hot.cu)
+  int sm = 0;                // CTA head bin: G > 0 = SM-shared head kernel (k_epoch_sm_tma, one CTA of G row groups per SM)
+  int sm_ch = 0;             // SM kernel: head chunks flushed per flushing row
+  int sm_rh = 1;             // SM kernel: rows per flushing row
   int snap = 0;              // 1 = every slice launch gathers from a copy of the shared vector taken just
                              // before it (the whole slice within the bin's staleness cap)
   int64_t count = 0, nnz = 0;
@@ -237,6 +240,8 @@ scd_status profile_collect(scd_ctx *c);
 scd_status tune_shared_layout(scd_ctx *c);
 void bin_launch_shape(scd_ctx *c, Bin &b);
 double combine_budget(const scd_ctx *c, const Bin &b);  // deferred-update budget of a bin (reading c25)
+bool sm_head_shape(scd_ctx *c, Bin &b);  // SM-shared head kernel shape (false = not used)
+int sm_chunk_entries();                  // SM-shared head kernel: entries per staged chunk
 double cap_fraction();  // in-flight cap as a fraction of a staleness bound (layout.cu)
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
 scd_status launch_block_order_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk,

@@ -414,6 +414,420 @@ __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, Bin
   head_flush<T>(a.sv, s_acc, H, b.dry);  // after the exit barrier: every pending update is final
 }
 
+// mbarrier + 1-D bulk copy (TMA) helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+
+// ----------------------------------------------------------------------------------------------
+// SM-shared head kernel with bulk-copied rows (default for the single head bin of a dual with the
+// rolling tail copy: C3; DESIGN.md §6 "SM-shared head kernel").
+//
+// One 1024-thread CTA per SM runs G = 4 row groups of T = 256 threads; a group does one row at a time.
+// The four rows an SM has in flight share one shared-memory state of the frequency-ranked head:
+//   S[0, H)  the SM's snapshot of w̄[0, H)
+//   P[0, H)  the SM's pending updates of w̄[0, H) (not yet reduced into w̄)
+// A head read is S[j] + P[j] (no L2 access; the head was ~620 L2 sector reads per C3 row), a tail read
+// (j >= H) is the rolling tail read copy svr[j].  Head scatters are shared-memory
+// compare-and-swap adds into P (the groups of an SM may hit the same entry), tail scatters red.global.add.
+// Rolling flush by the SM's row count u: every rh-th row flushes head chunks (u/rh·ch + k) mod nh, k < ch,
+// of 4T floats (exchange P with 0, one v4 RED per touched float4, S = the w̄ value loaded before that RED
+// plus the flushed part, so S + P stays w̄ + the SM's own pending).  A head read then misses at most
+// the other SMs' pending updates and what they flushed since its chunk's refresh, nh/ch·rh rows of every
+// other SM each: that joins the combined-update budget (reading c25; sm_head_shape).
+//
+// The row's entries are not held in registers: each group streams its row through two shared-memory
+// buffers of C entries (idx and val) filled by 1-D bulk copies (cp.async.bulk, completion on an mbarrier
+// with a transaction count; the row itself is prefetched into L2 by cp.async.bulk.prefetch when it is
+// published, a row ahead).  The gather-dot reads chunk i while chunk i + 1 is copied; the scatter walks
+// the chunks backwards, so the last two are still resident and only rows longer than 2C re-read chunks
+// (L2 hits); the buffers freed at the end of the scatter take the NEXT row's first two chunks, so a row
+// starts with its entries on chip.  A buffer is handed back by the last of the group's warps to read it
+// (shared-memory counter), which issues the next copy into it; the row descriptors and the partial sums
+// are double-buffered by row parity, every warp derives the delta itself: one group barrier per row.
+struct SmHeadArgs {
+  int H;   // head snapshot / pending extent [0, H), a multiple of 4 * T
+  int ch;  // head chunks flushed per flushing row
+  int rh;  // rows per flushing row
+};
+
+template <int T>
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(T) : "memory");
+}
+
+__device__ __forceinline__ float4 exch4_zero(float *p) {
+  float4 r;
+  r.x = atomicExch(p + 0, 0.f);
+  r.y = atomicExch(p + 1, 0.f);
+  r.z = atomicExch(p + 2, 0.f);
+  r.w = atomicExch(p + 3, 0.f);
+  return r;
+}
+
+__device__ __forceinline__ bool nonzero4(float4 v) { return v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f; }
+
+// Predicated accesses: the entries of a warp fall in both ranges (head / tail), and per-entry branches
+// serialise the warp over the paths and keep the compiler from batching the loads of several entries.
+__device__ __forceinline__ void red_if(float *p, float v, bool c) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.global.add.f32 [%0], %1; }" ::"l"(p), "f"(v), "r"((unsigned)c)
+               : "memory");
+}
+// shared-memory CAS issued only where c holds; returns the value seen (o itself where c is false)
+__device__ __forceinline__ unsigned cas_shared_if(float *p, unsigned o, unsigned n, bool c) {
+  unsigned r = o;
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %4, 0; @q atom.shared.cas.b32 %0, [%1], %2, %3; }"
+               : "+r"(r)
+               : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(o), "r"(n), "r"((unsigned)c)
+               : "memory");
+  return r;
+}
+
+// Shared-vector read of entry j: S[j] + P[j] for j < H, svr[j] beyond; the shared-memory and the L2
+// load land in one register under complementary predicates.  j < 0 (no entry) reads S[0] + P[0]; the
+// caller gives it a zero weight.
+__device__ __forceinline__ float sm_read(const float *S, const float *P, const float *svr, int H, int32_t j) {
+  float r, p;
+  const unsigned js = (unsigned)max(j, 0) * 4u;
+  asm("{ .reg .pred q; setp.lt.s32 q, %2, %3;\n\t"
+      "@q ld.shared.f32 %0, [%4];\n\t"
+      "@!q ld.global.cg.f32 %0, [%5];\n\t"
+      "mov.f32 %1, 0f00000000;\n\t"
+      "@q ld.shared.f32 %1, [%6]; }"
+      : "=f"(r), "=f"(p)
+      : "r"(j), "r"(H), "r"(smem_u32(S) + js), "l"(svr + j), "r"(smem_u32(P) + js));
+  return r + p;
+}
+
+// Scatter of 4 entries (id < 0 = none): ids < H into the SM's pending P, the rest with red.global.add.
+// The pending adds are compare-and-swap rounds issued for all 4 entries at once (an fp32 shared-memory
+// atomicAdd compiles to one CAS loop per entry, each waiting out two shared-memory round trips); another
+// group of the SM rarely hits the same entry at the same time, so the retry loop almost never runs.
+__device__ __forceinline__ void pend_scatter4(float *P, float *sv, int H, const int32_t *id, const float *v, float d) {
+  unsigned o[4];
+  bool pend[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    pend[q] = id[q] >= 0 && id[q] < H;
+    o[q] = __float_as_uint(P[min((unsigned)id[q], (unsigned)H - 1u)]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float dv = v[q] * d;
+    const unsigned r = cas_shared_if(P + id[q], o[q], __float_as_uint(__uint_as_float(o[q]) + dv), pend[q]);
+    red_if(sv + id[q], dv, id[q] >= H);
+    pend[q] = pend[q] && r != o[q];  // lost the race: retry from the value seen
+    o[q] = r;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    while (pend[q]) {
+      const unsigned n = __float_as_uint(__uint_as_float(o[q]) + v[q] * d);
+      const unsigned r = atomicCAS(reinterpret_cast<unsigned *>(P + id[q]), o[q], n);
+      pend[q] = r != o[q];
+      o[q] = r;
+    }
+}
+
+struct RowInfo {
+  int64_t c, beg, end, t;  // coordinate (-1 = none), its entries [beg, end), its position t
+  float x, nrm, y;         // x[c], norm[c], y[c]
+  unsigned u;              // SM row index
+};
+
+template <int C, int NW>
+struct alignas(16) GroupSmem {
+  int32_t idx[2][C + 4];
+  float val[2][C + 4];
+  uint64_t bar[2];
+  int64_t a0[2], a1[2];  // buffer b holds the stored entries [a0, a1) (16-byte aligned copy)
+  unsigned cnt[2];       // warps done with buffer b
+  RowInfo row[2];        // by row parity
+  RowInfo stg;           // the next row's loads land here (cp.async) until it is published
+  float red[2][NW];      // partial sums by row parity
+};
+
+// Prefetch the stored entries [gb, ge) of a row into L2 (bulk prefetch, no shared memory): its chunks'
+// bulk copies then hit L2 instead of DRAM.
+__device__ __forceinline__ void prefetch_row_l2(const EpochArgs &a, int64_t gb, int64_t ge) {
+  const int64_t a0 = gb & ~(int64_t)3;
+  int64_t a1 = (ge + 3) & ~(int64_t)3;
+  const int64_t lim = a.nnz & ~(int64_t)3;
+  if (a1 > lim) a1 = lim;
+  if (a1 <= a0) return;
+  const unsigned bytes = (unsigned)(a1 - a0) * 4u;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.idx + a0), "r"(bytes) : "memory");
+  if (a.val) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.val + a0), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Copy the entries [gb, ge) (at most C) into buffer bi (one thread).  The copy covers the 16-byte aligned
+// superset [gb & ~3, min(ceil4(ge), floor4(nnz))); entries past it (the last stored entries of the matrix
+// only) are read from global memory by the consumer.
+template <int C, int NW>
+__device__ __forceinline__ void issue_chunk(const EpochArgs &a, GroupSmem<C, NW> *gs, int bi, int64_t gb, int64_t ge) {
+  const int64_t a0 = gb & ~(int64_t)3;
+  int64_t a1 = (ge + 3) & ~(int64_t)3;
+  const int64_t lim = a.nnz & ~(int64_t)3;
+  if (a1 > lim) a1 = lim;
+  if (a1 < a0) a1 = a0;
+  gs->a0[bi] = a0;
+  gs->a1[bi] = a1;
+  const unsigned bytes = (unsigned)(a1 - a0) * 4u;
+  // the buffer was last read through the generic proxy (those reads are ordered before this thread by
+  // the hand-back counter and a CTA fence)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(&gs->bar[bi], a.val ? 2u * bytes : bytes);
+  if (bytes) {
+    bulk_g2s(gs->idx[bi], a.idx + a0, bytes, &gs->bar[bi]);
+    if (a.val) bulk_g2s(gs->val[bi], a.val + a0, bytes, &gs->bar[bi]);
+  }
+}
+
+template <int C, int NW>
+__device__ __forceinline__ void issue_row_chunk(const EpochArgs &a, GroupSmem<C, NW> *gs, int bi, const RowInfo &r, int i) {
+  const int64_t gb = r.beg + (int64_t)i * C;
+  issue_chunk<C, NW>(a, gs, bi, gb, min(r.end, gb + (int64_t)C));
+}
+
+// The warp is done reading buffer bi; the last warp of the group to get here issues the next copy into
+// it: chunk i + 2 after the gather-dot of chunk i (the last two chunks stay for the scatter), chunk i - 2
+// after the scatter of chunk i, the next row's chunk 0 / 1 after the scatter of chunk 1 / 0.
+template <int C, int NW>
+__device__ __forceinline__ void hand_back(const EpochArgs &a, GroupSmem<C, NW> *gs, int bi, int lane, bool scatter, int i,
+                                          int n, int par) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    if (atomicAdd(&gs->cnt[bi], 1u) == NW - 1) {
+      gs->cnt[bi] = 0;
+      __threadfence_block();
+      const RowInfo &cur = gs->row[par];
+      const RowInfo &nxt = gs->row[par ^ 1];
+      if (!scatter) {
+        if (i + 2 < n) issue_row_chunk<C, NW>(a, gs, bi, cur, i + 2);
+      } else if (i >= 2) {
+        issue_row_chunk<C, NW>(a, gs, bi, cur, i - 2);
+      } else if (nxt.c >= 0) {
+        const int nn = (int)((nxt.end - nxt.beg + C - 1) / C);
+        if (i == 1) issue_row_chunk<C, NW>(a, gs, bi, nxt, 0);
+        else if (nn >= 2) issue_row_chunk<C, NW>(a, gs, bi, nxt, 1);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// The U entries of this thread in chunk [cb, cb + ce) held by buffer bi (j = -1 past the chunk).
+template <int C, int NW, int T, int U>
+__device__ __forceinline__ void chunk_entries(const EpochArgs &a, const GroupSmem<C, NW> *gs, int bi, int64_t cb, int ce,
+                                              int gt, int32_t *j, float *v) {
+  const int off0 = (int)(cb - gs->a0[bi]), lim = (int)min(gs->a1[bi] - cb, (int64_t)C);
+#pragma unroll
+  for (int q = 0; q < U; ++q) {
+    const int k = q * T + gt;
+    j[q] = k < ce ? gs->idx[bi][off0 + k] : -1;
+    v[q] = a.val ? gs->val[bi][off0 + min(k, C - 1)] : 1.f;
+  }
+  if (lim < ce) {  // the chunk runs past the aligned copy: the matrix's last stored entries
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int k = q * T + gt;
+      if (k < ce && k >= lim) {
+        j[q] = __ldg(a.idx + cb + k);
+        v[q] = a.val ? __ldg(a.val + cb + k) : 1.f;
+      }
+    }
+  }
+}
+
+template <int FORM, int G, int T, int C>
+__global__ void __launch_bounds__(G *T, 1) k_epoch_sm_tma(EpochArgs a, BinArgs b, SmHeadArgs h) {
+  constexpr int NW = T / 32;
+  constexpr int CH = 4 * T;  // floats per flushed chunk (one float4 per thread of a group)
+  constexpr int U = C / T;   // entries per thread per chunk
+  static_assert(C % T == 0 && U % 4 == 0, "chunk shape");
+  extern __shared__ float4 s_dyn[];
+  float *S = reinterpret_cast<float *>(s_dyn);
+  float *P = S + h.H;
+  __shared__ unsigned s_rows;
+  const int tid = threadIdx.x, g = tid / T, gt = tid % T, lane = tid & 31, wl = gt >> 5;
+  const int H = h.H;
+  GroupSmem<C, NW> *gs = reinterpret_cast<GroupSmem<C, NW> *>(P + H) + g;
+  for (int i = tid * 4; i < H; i += G * T * 4) {
+    *reinterpret_cast<float4 *>(S + i) = __ldcg(reinterpret_cast<const float4 *>(a.sv + i));
+    *reinterpret_cast<float4 *>(P + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (tid == 0) s_rows = 0;
+  __syncthreads();
+  // group thread 0: fetch of the next coordinate (ticket taken a row earlier); its offsets, model value,
+  // norm and label are copied into gs->stg asynchronously (no registers held across the row)
+  int64_t n_c = -1, n_t = 0;
+  unsigned n_tk = 0;
+  auto fetch = [&](unsigned tk) {
+    n_t = b.lo + (int64_t)tk;
+    n_c = -1;
+    if (n_t >= b.hi) return;
+    n_c = bin_coord(b, n_t);
+    cp_async8(&gs->stg.beg, a.ptr + n_c);
+    cp_async8(&gs->stg.end, a.ptr + n_c + 1);
+    cp_async4(&gs->stg.x, a.x + n_c);
+    cp_async4(&gs->stg.nrm, a.norm + n_c);
+    if (FORM == SCD_DUAL) cp_async4(&gs->stg.y, a.y + n_c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto publish = [&](int slot) {  // the fetched row becomes gs->row[slot]; its entries go to L2
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    RowInfo &d = gs->row[slot];
+    d.c = n_c;
+    d.t = n_t;
+    if (n_c >= 0) {
+      d.beg = gs->stg.beg;
+      d.end = gs->stg.end;
+      d.x = gs->stg.x;
+      d.nrm = gs->stg.nrm;
+      d.y = FORM == SCD_DUAL ? gs->stg.y : 0.f;
+      d.u = atomicAdd(&s_rows, 1u);
+      prefetch_row_l2(a, d.beg, d.end);
+    }
+  };
+  if (gt == 0) {
+    mbar_init(&gs->bar[0], 1);
+    mbar_init(&gs->bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    gs->cnt[0] = gs->cnt[1] = 0;
+    fetch(ticket_async(b, 1u));
+    n_tk = ticket_async(b, 1u);
+    publish(0);
+    const RowInfo &r0 = gs->row[0];
+    if (r0.c >= 0) {
+      issue_row_chunk<C, NW>(a, gs, 0, r0, 0);
+      if (r0.end - r0.beg > C) issue_row_chunk<C, NW>(a, gs, 1, r0, 1);
+    }
+  }
+  __syncthreads();
+  const int nh = H / CH;
+  unsigned ph = 0;  // mbarrier phase parity of the two buffers (bit b)
+  int b0 = 0;       // buffer holding the current row's first chunk
+  for (int par = 0;; par ^= 1) {
+    const RowInfo &r = gs->row[par];  // read from shared memory where used
+    const int64_t rc = r.c;
+    if (rc < 0) break;
+    const int64_t beg = r.beg, end = r.end;
+    const int n = (int)((end - beg + C - 1) / C);
+    if (gt == 0) {  // the next row: its loads overlap this row's gather-dot
+      fetch(n_tk);
+      n_tk = ticket_async(b, 1u);
+    }
+    if (a.roll_R > 0 && !b.dry && r.t % a.roll_R == 0) {
+      // rolling tail copy: row position t refreshes chunk (t / roll_R) mod nchunks of svr
+      const int64_t nch = (a.roll_hi - a.roll_lo + CH - 1) / CH;
+      const int64_t i = a.roll_lo + ((r.t / a.roll_R) % nch) * CH + (int64_t)gt * 4;
+      float *dst = const_cast<float *>(a.svr);
+      if (i + 3 < a.roll_hi)
+        *reinterpret_cast<float4 *>(dst + i) = __ldcg(reinterpret_cast<const float4 *>(a.sv + i));
+      else
+        for (int64_t q = i; q < a.roll_hi && q < i + 4; ++q) dst[q] = __ldcg(a.sv + q);
+    }
+    // the head chunk this row refreshes: its w̄ value is loaded now, consumed after the gather-dot
+    const bool hfl = r.u % (unsigned)h.rh == 0;
+    const unsigned hq = (r.u / (unsigned)h.rh) * (unsigned)h.ch;
+    const int ih = (int)(hq % (unsigned)nh) * CH + gt * 4;
+    float4 cur = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (hfl) cur = __ldcg(reinterpret_cast<const float4 *>(a.sv + ih));
+    // gather-dot over the chunks
+    float acc = 0.f;
+    for (int i = 0; i < n; ++i) {
+      const int bi = (b0 + i) & 1;
+      mbar_wait(&gs->bar[bi], (ph >> bi) & 1u);
+      ph ^= 1u << bi;
+      const int64_t cb = beg + (int64_t)i * C;
+      int32_t j[U];
+      float v[U], w[U];
+      chunk_entries<C, NW, T, U>(a, gs, bi, cb, (int)min((int64_t)C, end - cb), gt, j, v);
+      // the entries are in registers: hand the buffer back before the gathers (the next copy into it
+      // then overlaps their round trip)
+      hand_back<C, NW>(a, gs, bi, lane, false, i, n, par);
+#pragma unroll
+      for (int q = 0; q < U; ++q) w[q] = sm_read(S, P, a.svr, H, j[q]);
+#pragma unroll
+      for (int q = 0; q < U; ++q) acc = fmaf(w[q], j[q] >= 0 ? v[q] : 0.f, acc);
+    }
+    // rolling flush of the SM's pending head; S refreshed from the value loaded before the RED
+    if (hfl) {
+      for (int k = 0; k < h.ch; ++k) {
+        const int ik = (int)((hq + (unsigned)k) % (unsigned)nh) * CH + gt * 4;
+        const float4 ck = k == 0 ? cur : __ldcg(reinterpret_cast<const float4 *>(a.sv + ik));
+        const float4 pk = exch4_zero(P + ik);
+        if (nonzero4(pk)) red_add_v4(a.sv + ik, pk);
+        *reinterpret_cast<float4 *>(S + ik) = make_float4(ck.x + pk.x, ck.y + pk.y, ck.z + pk.z, ck.w + pk.w);
+      }
+    }
+    if (gt == 0) publish(par ^ 1);  // the next row (read after the barrier below)
+    acc = warp_sum(acc);
+    if (lane == 0) gs->red[par][wl] = acc;
+    group_sync<T>(g);
+    // every warp sums the partials and derives the same delta (no second barrier)
+    float sum = lane < NW ? gs->red[par][lane] : 0.f;
+    sum = warp_sum(sum);
+    float d = 0.f;
+    if (lane == 0) d = coord_delta<FORM>(sum, r.x, r.nrm, r.y, a.lam, a.lamN);
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (gt == 0 && !b.dry) a.x[rc] = r.x + d;  // single writer per epoch (c10)
+    d = b.dry ? 0.f : scatter_scale<FORM>(d);
+    // a one-chunk row leaves the other buffer free from here on: the next row's first chunk goes there
+    if (n == 1 && gt == 0 && n_c >= 0) issue_row_chunk<C, NW>(a, gs, b0 ^ 1, gs->row[par ^ 1], 0);
+    // scatter, chunks in reverse order (the last two are still resident)
+    for (int i = n - 1; i >= 0; --i) {
+      const int bi = (b0 + i) & 1;
+      if (i <= n - 3) {  // re-read (issued when chunk i + 2 was handed back)
+        mbar_wait(&gs->bar[bi], (ph >> bi) & 1u);
+        ph ^= 1u << bi;
+      }
+      const int64_t cb = beg + (int64_t)i * C;
+      int32_t j[U];
+      float v[U];
+      chunk_entries<C, NW, T, U>(a, gs, bi, cb, (int)min((int64_t)C, end - cb), gt, j, v);
+      hand_back<C, NW>(a, gs, bi, lane, true, i, n, par);
+      if (d != 0.f || b.dry) {
+#pragma unroll
+        for (int q0 = 0; q0 < U; q0 += 4) pend_scatter4(P, a.sv, H, j + q0, v + q0, d);
+      }
+    }
+    b0 ^= 1;  // the next row's first chunk went into the other buffer
+  }
+  __syncthreads();  // every group has left its loop: the pending updates are final
+  for (int i = tid * 4; i < H; i += G * T * 4) {
+    const float4 p = *reinterpret_cast<const float4 *>(P + i);
+    if (nonzero4(p)) red_add_v4(a.sv + i, p);
+  }
+}
+
 // ----------------------------------------------------------------------------------------------
 template <int FORM, int G, int E, bool WILD = false>
 __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
@@ -972,29 +1386,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster(
 // coordinate is known one iteration early: CTA 0 takes its ticket while the current one is reduced
 // and publishes it with the delta.  Three cluster barriers per coordinate (previous scatter done,
 // partials, delta), as in k_epoch_cluster.
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
-  unsigned done = 0;
-  while (!done)
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-}
-
 struct Slice {
   int64_t beg, end;  // the CTA's entries [beg, end) of the coordinate
   int64_t st;        // entries [beg, beg + st) are staged in shared memory, from offset off of the buffer
@@ -1130,6 +1521,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster_
 
 // kernel table ---------------------------------------------------------------------------------
 constexpr int kCtaT = kLanesCta, kCtaE = 16;
+constexpr int kSmG = 4, kSmC = 2048;  // SM-shared head kernel: row groups per SM, entries per staged chunk
 constexpr int kGrpE8 = 8, kGrpE32 = 16;
 constexpr int kClE = 8;
 constexpr int kCombT = 128, kCombS = 2048;  // CTA-combining kernel for 8-lane bins
@@ -1205,6 +1597,8 @@ void *bin_kernel(const scd_ctx *c, const Bin &b) {
     return c->opt.wild ? cluster_kernel<SCD_DUAL, true>(false) : cluster_kernel<SCD_DUAL, false>(tma);
   }
   if (c->opt.wild) return c->form == SCD_PRIMAL ? kernel_wild<SCD_PRIMAL>(b.lanes) : kernel_wild<SCD_DUAL>(b.lanes);
+  if (b.head > 0 && b.lanes == kLanesCta && b.sm && c->form == SCD_DUAL && c->tail_snap)
+    return (void *)k_epoch_sm_tma<SCD_DUAL, kSmG, kCtaT, kSmC>;
   if (b.head > 0 && b.lanes == kLanesCta) {
     // the read copies exist only for the dual (setup_tail_snap); the head copy needs the rolling tail copy
     if (c->form == SCD_DUAL && c->tail_snap && c->head_copy > 0)
@@ -1395,6 +1789,61 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   }
 }
 
+// Dynamic shared memory of a bin's kernel.
+size_t bin_smem(const scd_ctx *c, const Bin &b) {
+  if (b.hot > 0) return 8 * (size_t)b.hot;
+  if (b.head > 0 && b.sm) return 2 * sizeof(float) * (size_t)b.head + kSmG * sizeof(GroupSmem<kSmC, kCtaT / 32>);
+  if (b.head > 0) return sizeof(float) * (size_t)b.head;
+  return b.lanes == kLanesCluster ? cluster_smem(c) : 0;
+}
+
+// SM-shared head kernel (k_epoch_sm_tma) for the single head bin of a dual with the rolling tail copy
+// (build_schedule): one CTA of kSmG row groups per SM.  Its head staleness (reading c25): rows in flight
+// (nsm·G) + 2·nsm·Q (the other SMs' pending head and what they flushed since a chunk's snapshot, Q rows
+// of each, Q = nh/ch·rh the rows between two refreshes of a chunk) <= the combined-update budget.  ch is
+// the smallest chunk count per flushing row that fits, then rh the largest period (<= 8).  The kernel's
+// head is the bin's head (the tail copy starts there).  SCD_SM_HEAD=0 keeps k_epoch_cta_head.
+// Returns false when it does not fit (then k_epoch_cta_head runs).
+bool sm_head_shape(scd_ctx *c, Bin &b) {
+  b.sm = 0;
+  const char *e = getenv("SCD_SM_HEAD");
+  if ((e && atoi(e) == 0) || b.head <= 0 || b.lanes != kLanesCta || c->form != SCD_DUAL) return false;
+  constexpr int CH = 4 * kCtaT;
+  if (b.head % CH != 0) return false;
+  const int64_t inflight = (int64_t)c->nsm * kSmG;
+  if (b.cap > 0 && inflight > b.cap) return false;
+  const double budget = combine_budget(c, b);
+  const int nh = b.head / CH;
+  auto fits = [&](double q) { return (double)inflight + 2.0 * (double)c->nsm * q <= budget; };
+  int ch = 0, rh = 1;
+  for (int k = 1; k <= nh; k *= 2)
+    if (fits((double)((nh + k - 1) / k))) {
+      ch = k;
+      break;
+    }
+  if (ch == 0) return false;
+  if (ch == 1)
+    while (rh < 8 && fits((double)nh * (rh + 1))) ++rh;
+  b.sm = kSmG;
+  b.sm_ch = ch;
+  b.sm_rh = rh;
+  void *fn = bin_kernel(c, b);
+  const size_t smem = bin_smem(c, b);
+  int occ = 0;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kSmG * kCtaT, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    b.sm = 0;
+    return false;
+  }
+  b.grid = c->nsm;
+  b.block = kSmG * kCtaT;
+  b.flush = 0;
+  return true;
+}
+
+int sm_chunk_entries() { return kSmC; }
+
 // Launch one bin's kernel over the permutation positions [ba.lo, ba.hi) with `grid` CTAs.
 scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64_t grid, cudaStream_t s) {
   void *fn = bin_kernel(c, b);
@@ -1402,7 +1851,9 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
   void *args_head[] = {&a, &ba, &H, &F};
   HotArgs ha;
   void *args_hot[] = {&a, &ba, &ha};
-  void **args = args_head;
+  SmHeadArgs sh{b.head, b.sm_ch, b.sm_rh};
+  void *args_sm[] = {&a, &ba, &sh};
+  void **args = b.sm ? args_sm : args_head;
   if (b.hot > 0 && b.lanes == 8 && !c->opt.wild) {
     ha.idx = c->hot_idx;
     ha.hot_ids = c->hot_ids;
@@ -1412,8 +1863,7 @@ scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64
     ha.P = (int)std::max<int64_t>(1, c->hot_copy);
     args = args_hot;
   }
-  const size_t smem = b.hot > 0 ? 8 * (size_t)b.hot
-                     : (b.head > 0 ? sizeof(float) * (size_t)b.head : (b.lanes == kLanesCluster ? cluster_smem(c) : 0));
+  const size_t smem = bin_smem(c, b);
   if (smem >= 48 * 1024) SCD_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SCD_CK(c, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(b.block), args, smem, s));
   return SCD_OK;
@@ -1531,7 +1981,7 @@ scd_status tune_shared_layout(scd_ctx *c) {
   if (bi < 0) return SCD_OK;
   Bin &b = c->bins[bi];
   cudaStream_t s = c->stream;
-  const int cpc = b.lanes <= 32 ? b.block / b.lanes : 1;
+  const int cpc = b.lanes <= 32 ? b.block / b.lanes : (b.sm ? b.sm : 1);
   const int64_t probe = std::min<int64_t>(b.count, (int64_t)b.grid * cpc * 8);  // ~0.14 ms per C3 probe launch
   SCD_CK(c, cudaMemsetAsync(c->sv_base, 0, sizeof(float) * (size_t)(c->n_shared + kMaxSvOffsetFloats), s));
   // all probe launches enqueued back to back between events (one warm-up, then kReps per candidate

@@ -608,13 +608,18 @@ scd_status build_schedule(scd_ctx *c) {
       // With several bins (or SCD_SLICES) the copy is refreshed between slices instead.
       c->tail_roll = 0;
       if (c->n_bins == 1 && S_env == 0 && c->opt.max_inflight == 0) {
-        const Bin &B = c->bins[bi];
+        Bin &B = c->bins[bi];
         const int64_t nch = (c->tail_hi - c->tail_lo + 4 * kLanesCta - 1) / (4 * kLanesCta);
         const double sweep = std::min(cap_fraction() * c->tail_tau, (double)B.count / 8.0);
         const int64_t R = nch > 0 ? (int64_t)(sweep / (double)nch) : 0;
         if (R >= 1) {
           c->tail_roll = R;
           S = 1;
+          // one launch per epoch with the rolling copy: the SM-shared head kernel when its window fits
+          if (!sm_head_shape(c, B) && B.sm) {
+            B.sm = 0;
+            bin_launch_shape(c, B);
+          }
         }
       }
       // Head copy: the head gathers also read svr[0, H), refreshed in rolling 1024-float chunks every
@@ -624,7 +629,7 @@ scd_status build_schedule(scd_ctx *c) {
       // gives way (down to 2) until P >= 16 fits (a shorter period costs more in refresh traffic than
       // it saves: profiles/head_copy_r1.txt).
       Bin &HB = c->bins[bi];
-      if (c->tail_roll > 0 && HB.head > 0) {
+      if (c->tail_roll > 0 && HB.head > 0 && !HB.sm) {
         const int64_t nchh = (HB.head + 4 * kLanesCta - 1) / (4 * kLanesCta);
         const double budget = combine_budget(c, HB);
         int64_t P = 0;

@@ -115,11 +115,11 @@ def _side_by_side(form: str, band: float, envelope: str, cfg=None, seed: int = 3
 
 
 def test_c3_dual_full_size_against_oracle():
-    """Bench schedule on C3 (k_epoch_cta_head, one launch per epoch): per-epoch gap within 1.25x of the
+    """Bench schedule on C3 (k_epoch_sm_tma, one launch per epoch): per-epoch gap within 1.25x of the
     sequential fp64 SDCA's envelope over 4 seeds (measured <= 1.07x), optimum to 1e-5."""
     A, alpha, wbar, info = _side_by_side("dual", BAND, "C3")
     b = info["bins"][0]
-    assert len(info["bins"]) == 1 and b["head"] > 0 and info["tail_roll"] > 0, info  # the benchmarked kernel
+    assert len(info["bins"]) == 1 and b["head"] > 0 and info["tail_roll"] > 0 and info["sm_head"] > 0, info  # the bench kernel
     # shared-vector consistency on the active features (fp32 accumulation drift)
     v = A.T @ alpha
     act = np.nonzero(v)[0]

@@ -1,8 +1,10 @@
 """GPU: the webspam-shaped CTA-bin kernels against the fp64 oracle.
 
-  * k_epoch_cta_head (default for the C3-shaped dual): each CTA combines its updates of the dense head
-    of w̄ in shared memory and flushes them every `flush` rows; the extra staleness is bounded by the
-    schedule (grid * (1 + flush) <= τ).
+  * k_epoch_sm_tma (default for the C3-shaped dual): one CTA of 4 row groups per SM shares a snapshot
+    of the dense head of w̄ and its pending updates (flushed chunk by chunk); rows are staged in shared
+    memory by bulk copies.  Extra staleness bounded by the schedule (reading c25).
+  * k_epoch_cta_head (SCD_SM_HEAD=0 and the fallback): each CTA combines its updates of the dense head
+    of w̄ in shared memory and flushes them every `flush` rows (grid * (1 + flush) <= τ).
   * k_epoch_group_hot (default for criteo-shaped one-hot rows): the measured hot set combined per CTA.
 
 Input: the first 20 000 rows of C3 (BASELINE configs[2]; row generation is independent per row, so
@@ -47,6 +49,7 @@ def _converge(d, pr, hist, env):
         s.epoch(t)
         gaps.append(s.duality_gap())
     x = s.get_model().astype(np.float64)
+    wbar = s.get_shared().astype(np.float64)
     s.close()
     A = pr.A()
     Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
@@ -57,26 +60,49 @@ def _converge(d, pr, hist, env):
     assert abs(Pg - Pstar) <= 1e-5 * abs(Pstar), (Pg, Pstar)
     assert gaps[-1] <= 1e-5
     check_stress_band(gaps, *env, label="c3 prefix")
+    # every deferred (combined / pending) update reached the shared vector: w̄ = Aᵀα up to fp32 drift
+    v = A.T @ x
+    drift = np.abs(wbar - v).max() / np.abs(v).max()
+    print("shared-vector drift %.2e" % drift)
+    assert drift <= 1e-4, drift
     return info
 
 
-def test_head_kernel_schedule_and_convergence(c3p, monkeypatch):
+def _tail_copy_asserts(info, b, c3p):
+    # single head bin: the tail copy is refreshed in rolling chunks inside one launch per epoch; a full
+    # sweep (R rows per 1024-float chunk) stays within half the tail coupling's bound and 1/8 of the bin
+    assert info["tail_snap"] == 1 and info["tail_roll"] >= 1 and info["n_slices"] == 1, info
+    nch = -(-(int(c3p[0]["idx"].max()) + 1 - b["head"]) // 1024)
+    assert info["tail_roll"] * nch <= min(0.5 * info["tail_tau"], b["count"] / 8), (info["tail_roll"], nch)
+
+
+def test_sm_head_kernel_schedule_and_convergence(c3p, monkeypatch):
+    """Default for the C3-shaped dual: k_epoch_sm_tma (one CTA of 4 row groups per SM sharing the head
+    snapshot and its pending updates, rows staged in shared memory by bulk copies)."""
     monkeypatch.delenv("SCD_HEAD", raising=False)
+    monkeypatch.delenv("SCD_SM_HEAD", raising=False)
+    info = _converge(*c3p)
+    b = [b for b in info["bins"] if b["lanes"] == 256][0]
+    assert info["sm_head"] == 4 and b["grid"] == 148 and b["block"] == 1024 and b["head"] == 8192, info
+    # rows in flight + the other SMs' pending head and what they flushed since a chunk's refresh
+    # (nh / ch * rh rows of each SM) within the combined-update budget (reading c25)
+    q = (b["head"] // 1024) // info["sm_ch"] * info["sm_rh"]
+    assert b["grid"] * info["sm_head"] + 2 * b["grid"] * q <= min(b["tau"], b["count"] / 8), info
+    _tail_copy_asserts(info, b, c3p)
+
+
+def test_cta_head_kernel_schedule_and_convergence(c3p, monkeypatch):
+    """k_epoch_cta_head (SCD_SM_HEAD=0, and wherever the SM-shared kernel's window does not fit)."""
+    monkeypatch.delenv("SCD_HEAD", raising=False)
+    monkeypatch.setenv("SCD_SM_HEAD", "0")
     info = _converge(*c3p)
     cta = [b for b in info["bins"] if b["lanes"] == 256]
-    assert cta, info
+    assert cta and info["sm_head"] == 0, info
     b = cta[0]
     assert b["head"] == 8192 and b["flush"] >= 2, b
     # rows in flight + pending head updates of `flush` rows per CTA: bounded by the staleness bound
     assert b["grid"] * (1 + b["flush"]) <= b["tau"], b
-    # tail read copy: only while one slice of the bin stays within half the tail coupling's bound
-    if info["tail_snap"]:
-        assert b["count"] / info["n_slices"] <= 0.5 * info["tail_tau"], info
-    # single head bin: the copy is refreshed in rolling chunks inside one launch per epoch; a full
-    # sweep (R rows per 1024-float chunk) stays within the same bounds as a slice
-    assert info["tail_snap"] == 1 and info["tail_roll"] >= 1 and info["n_slices"] == 1, info
-    nch = -(-(int(c3p[0]["idx"].max()) + 1 - b["head"]) // 1024)
-    assert info["tail_roll"] * nch <= min(0.5 * info["tail_tau"], b["count"] / 8), (info["tail_roll"], nch)
+    _tail_copy_asserts(info, b, c3p)
     # head copy: rows in flight + deferred + the copy's age stay within the combined-update budget
     if info["head_copy"]:
         age = info["head_copy"] * -(-b["head"] // 1024)

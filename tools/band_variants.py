@@ -38,7 +38,8 @@ def child(which, E):
         out.append((e0.elapsed_time(e1), s.duality_gap()))
     info = s.info()
     s.close()
-    print("RESULT " + json.dumps(dict(rows=out, bins=info["bins"], n_slices=info["n_slices"])))
+    print("RESULT " + json.dumps(dict(rows=out, bins=info["bins"], n_slices=info["n_slices"],
+                                      sm={k: info.get(k) for k in ("sm_head", "sm_chunk", "sm_ch", "sm_rh", "tail_roll", "head_copy")})))
 
 
 def main():
@@ -61,7 +62,7 @@ def main():
         ms = sum(x[0] for x in res["rows"][1:]) / max(1, len(res["rows"]) - 1)
         ratios = " ".join(f"{g / o:.2f}" for (_, g), o in zip(res["rows"], orc))
         gaps = " ".join(f"{g:.2e}" for _, g in res["rows"])
-        print(f"{var or '(default)':40s} {ms:7.2f} ms/epoch  gaps {gaps}  ratio {ratios}", flush=True)
+        print(f"{var or '(default)':40s} {ms:7.2f} ms/epoch  gaps {gaps}  ratio {ratios}  {res.get('sm')}", flush=True)
 
 
 if __name__ == "__main__":

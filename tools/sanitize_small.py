@@ -80,12 +80,18 @@ for env in ({}, {"SCD_TAIL_SNAP": "1"}, {"SCD_TAIL_SNAP": "0"}):
     for k in env:
         del os.environ[k]
 # rolling refresh of the tail copy (one head-kernel launch per epoch): needs a bin of >= 8 x 657 rows
+# (default: the SM-shared head kernel with bulk-copied rows; SCD_SM_HEAD=0: the per-CTA head kernel)
 c3r = synth.gen_host(synth.CONFIGS["C3"].with_rows(20_000))
 c3r["lam"] = 350.0 / 20_000
-s = scd.Solver(c3r["ptr"], c3r["idx"], c3r["val"], 20_000, c3r["n_cols"], c3r["y"], c3r["lam"], "dual", seed=3)
-inf = s.info()
-s.close()
-print("c3 rolling", inf["bins"][0], "tail_roll", inf["tail_roll"], run(c3r, "dual"), flush=True)
+for env in ({}, {"SCD_SM_HEAD": "0"}):
+    os.environ.update(env)
+    s = scd.Solver(c3r["ptr"], c3r["idx"], c3r["val"], 20_000, c3r["n_cols"], c3r["y"], c3r["lam"], "dual", seed=3)
+    inf = s.info()
+    s.close()
+    print("c3 rolling", env, inf["bins"][0], "tail_roll", inf["tail_roll"], "sm_head", inf["sm_head"], inf["sm_ch"],
+          inf["sm_rh"], run(c3r, "dual"), flush=True)
+    for k in env:
+        del os.environ[k]
 # criteo-shaped rows with λN = 2e5 (as in the 8-GPU shards): the hot-set kernel, explicit and implicit values
 c5h = synth.gen_host(synth.CONFIGS["C5"].with_rows(1_000_000))
 c5h["lam"] = 0.2
