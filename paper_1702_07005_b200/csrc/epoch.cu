@@ -1186,14 +1186,12 @@ __global__ void __launch_bounds__(T, 1) k_epoch_group_hot(EpochArgs a, BinArgs b
       }
       d = scatter_scale<FORM>(__shfl_sync(FULL, d, sub * G));
       if (d != 0.f || b.dry) {  // dry probe: same traffic, adds +0.0f
+        // tail entries: predicated REDs (no per-entry branch); hot entries: shared-memory adds
+#pragma unroll
+        for (int e = 0; e < E; ++e) red_if(a.sv + cur.id[e], cur.v[e] * d, (cur.valid >> e & 1) && cur.id[e] >= 0);
 #pragma unroll
         for (int e = 0; e < E; ++e)
-          if (cur.valid >> e & 1) {
-            if (cur.id[e] >= 0)
-              red_add(a.sv + cur.id[e], cur.v[e] * d);
-            else
-              atomicAdd(s_pend + (cur.id[e] & 0x7fffffff), cur.v[e] * d);
-          }
+          if ((cur.valid >> e & 1) && cur.id[e] < 0) atomicAdd(s_pend + (cur.id[e] & 0x7fffffff), cur.v[e] * d);
       }
       more = have_next;
       if (have_next) {

@@ -12,7 +12,8 @@ import os
 
 import numpy as np
 
-_SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libscd.so")
+# SCD_LIBSCD: another build of the same library (A/B measurements of kernel changes, tools/)
+_SO = os.environ.get("SCD_LIBSCD") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libscd.so")
 
 PRIMAL, DUAL = 0, 1
 AGG = {"add": 0, "average": 1, "optimal": 2}
