@@ -14,7 +14,8 @@ scaling, global N in λN).  The gap evaluation (a7) is off the clock, as in the 
 Sub-records on the same JSON line:
   N = 1: "c4_primal" (configs[3] at K = 1: C3's matrix by feature) and "c5_shard" (one GPU's
          25 M-row shard of configs[4], implicit values), each with its epoch time, nnz/s and the
-         roofline of its dominant kernel.
+         roofline of its dominant kernel; "c3_load" (the data layer at full scale: C3 with scattered
+         feature ids renumbered by frequency on the device by scd_renumber, then epochs on the result).
   N > 1: "north_star" — configs[4] criteo-shaped, weak-scaled at 25 M rows per rank (the full
          200 M x 75 M at N = 8), dual by example, time and rounds to gap 1e-4 with optimal γ and with
          the add / average baselines; and configs[3] C4 primal by feature at K = N.
@@ -515,6 +516,62 @@ def leg_c3(args, ctx):
     return rec, d
 
 
+def leg_load(args, ctx, d):
+    """The data layer at full scale ("ids scattered over 16.6 M and renumbered at load"):
+    C3's feature ids are scattered by a random bijection of [0, M) (rows no longer sorted, no frequency
+    order), scd_renumber restores a frequency ranking on the device, and the epoch runs on the result.
+    Checks: the renumbered per-feature counts are non-increasing, equal to the generator's as a multiset,
+    every row strictly increasing; epoch time on the renumbered matrix vs the headline's."""
+    torch = ctx.torch
+    import synth
+    import paper_1702_07005_b200 as scd
+
+    cfg = synth.CONFIGS["C3"]
+    N, M = cfg.n_rows, cfg.n_cols
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1234)
+    perm = torch.randperm(M, generator=g, device="cuda", dtype=torch.int64).to(torch.int32)
+    idx_s = perm.index_select(0, d["idx"]).contiguous()
+    del perm
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rp, ri, rv, new_of_old = scd.renumber(d["ptr"], idx_s, d["val"], N, M, "csr")
+    e1.record()
+    torch.cuda.synchronize()
+    ren_ms = e0.elapsed_time(e1)
+    del idx_s
+    cnt_r = torch.bincount(ri.long(), minlength=M)
+    cnt_o = torch.bincount(d["idx"].long(), minlength=M)
+    monotone = bool((cnt_r[1:] <= cnt_r[:-1]).all().item())
+    same_counts = bool(torch.equal(torch.sort(cnt_r, descending=True).values, torch.sort(cnt_o, descending=True).values))
+    rows_sorted = True
+    nnz = int(rp[-1].item())
+    diff = ri[1:].long() - ri[:-1].long()
+    starts = torch.zeros(nnz, dtype=torch.bool, device="cuda")
+    starts[rp[1:-1]] = True  # positions that begin a row
+    rows_sorted = bool(((diff > 0) | starts[1:]).all().item())
+    del cnt_r, cnt_o, diff, starts
+    s = scd.Solver(rp, ri, rv, N, M, d["y"], cfg.lam, "dual", seed=3, profile=True)
+    stream = torch.cuda.ExternalStream(s.stream_handle)
+    info = s.info()
+    for t in range(1, 4):
+        s.epoch(t)
+    torch.cuda.synchronize()
+    el = timed_epochs(ctx, s, stream, 4, 5, lambda t: s.epoch(t))
+    gap = s.duality_gap()
+    s.close()
+    del rp, ri, rv, new_of_old
+    torch.cuda.empty_cache()
+    return {"workload": "C3 with feature ids scattered by a random bijection, renumbered by frequency on the device "
+                        "(scd_renumber), then the dual epochs on the renumbered matrix",
+            "renumber_ms": ren_ms, "nnz": nnz,
+            "checks": {"counts_non_increasing": monotone, "counts_equal_generator_multiset": same_counts,
+                       "rows_strictly_increasing": rows_sorted},
+            "epoch_ms": el / 5, "gap_after_8_epochs": gap, "sm_head": info.get("sm_head"),
+            "head": info["bins"][0].get("head") if info["bins"] else None}
+
+
 def leg_c4(args, ctx, d):
     """configs[3]: C3's matrix by feature.  N = 1: K = 1 epochs (roofline of the dominant bin, time to
     1e-4).  N > 1: columns partitioned across the ranks (balanced partition, c29), optimal γ rounds."""
@@ -683,6 +740,12 @@ def main():
                 subs["c4_primal"] = leg_c4(args, ctx, d)
             except Exception as ex:
                 subs["c4_primal"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+            torch.cuda.empty_cache()
+            try:
+                subs["c3_load"] = leg_load(args, ctx, d)
+            except Exception as ex:
+                subs["c3_load"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+            torch.cuda.empty_cache()
             oracle_ttg = None
             if rank == 0 and not args.quick and not args.no_cpu_baseline:
                 try:
