@@ -242,12 +242,6 @@ typedef struct {
   int32_t sm_ch;          /* SM-shared head kernel: head chunks (1024 floats) flushed and re-read per flushing row */
   int32_t sm_rh;          /* SM-shared head kernel: rows per flushing row (an SM's head chunk rotates every
                              bin_head / 1024 / sm_ch * sm_rh of its rows) */
-  int32_t own;            /* > 0: the epoch runs the owner-computes kernel: w̄ partitioned over this many CTAs (one
-                             per SM, feature j owned by CTA j mod own, kept in its shared memory), the entries
-                             regrouped by owner at create; 0 = off */
-  int32_t own_warps;      /* owner-computes kernel: warps per owner CTA */
-  int32_t own_err;        /* owner-computes kernel: 1 if a wait for a published delta ever timed out (never
-                             expected; the epoch's result is then invalid) */
 } scd_info;
 scd_status scd_get_info(scd_ctx *c, scd_info *info);
 

@@ -68,13 +68,6 @@ void free_ctx(scd_ctx *c) {
   cudaFree(c->comm);
   for (void *p : c->p2p_open) cudaIpcCloseMemHandle(p);
   cudaFree(c->p2p_ptrs);
-  cudaFree(c->own_offs);
-  cudaFree(c->own_lidx);
-  cudaFree(c->own_lval);
-  cudaFree(c->own_part);
-  cudaFree(c->own_cnt);
-  cudaFree(c->own_dlt);
-  cudaFree(c->own_err);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto &p : c->ev_pending) {
     cudaEventDestroy(p.second.first);
@@ -343,7 +336,7 @@ scd_status scd_create(const scd_matrix *A, const float *y, scd_mem y_mem, double
       if (off > kMaxSvOffsetFloats) off = kMaxSvOffsetFloats;
       c->sv = c->sv_base + off;
       c->sv_offset_bytes = off * 4;
-    } else if (!opt.deterministic && c->n_bins > 0 && c->nnz >= (int64_t)20000000 && !(tn && atoi(tn) == 0) && !c->own) {
+    } else if (!opt.deterministic && c->n_bins > 0 && c->nnz >= (int64_t)20000000 && !(tn && atoi(tn) == 0)) {
       if ((st = tune_shared_layout(c)) != SCD_OK) return bail(st);
     }
   }
@@ -536,13 +529,6 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   info->hot_tp = c->hot_tp ? 1 : 0;
   info->hot_hp = (c->hot_hp && c->hot_copy > 0 && c->hot_tp) ? 1 : 0;
   info->hot_tail_tau = c->hot_tail_tau;
-  info->own = c->own;
-  info->own_warps = c->own_w;
-  info->own_err = 0;
-  if (c->own_err) {
-    cudaMemcpyAsync(&info->own_err, c->own_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
-    cudaStreamSynchronize(c->stream);
-  }
   info->sm_head = info->sm_chunk = info->sm_ch = info->sm_rh = 0;
   for (int i = 0; i < c->n_bins && i < 4; ++i)
     if (c->bins[i].sm) {

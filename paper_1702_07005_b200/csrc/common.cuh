@@ -180,19 +180,6 @@ struct scd_ctx {
   double tail_tau = 0.0;              // staleness bound of the head bin's coupling through the tail entries
   int64_t tail_roll = 0;              // > 0: the tail copy is refreshed chunk by chunk inside the epoch (every
                                       // tail_roll-th row one 1024-float chunk) instead of between slices
-  // owner-computes dual epoch: w̄ partitioned over `own` CTAs (one per SM), feature j
-  // owned by CTA j mod own at local index j / own, held in its shared memory during the epoch; the
-  // stored entries regrouped by owner (layout.cu setup_owner)
-  int own = 0;                    // > 0: the epoch runs k_epoch_owner on `own` CTAs
-  int own_L = 0;                  // local features per owner CTA
-  int own_w = 0;                  // warps per owner CTA
-  int64_t *own_offs = nullptr;    // [own][n_coord + 1]: start of coordinate n's entries owned by k
-  int32_t *own_lidx = nullptr;    // [nnz]: local feature index j / own
-  float *own_lval = nullptr;      // [nnz] (nullptr with implicit values)
-  float *own_part = nullptr;      // [n_coord]: partial dot products by epoch position
-  unsigned *own_cnt = nullptr;    // [n_coord]: owners arrived, by epoch position
-  float *own_dlt = nullptr;       // [n_coord]: coordinate deltas by epoch position (NaN = not yet)
-  int *own_err = nullptr;         // [1]: a spin wait timed out
   std::string err;
 };
 
@@ -262,11 +249,6 @@ scd_status launch_block_order_export(uint64_t seed, uint32_t epoch, uint32_t str
 scd_status partition_balanced_device(const int64_t *ptr, int64_t n, uint64_t seed, int32_t k, int32_t *d_owner,
                                      cudaStream_t s, std::string &err);
 scd_status launch_partition_export(uint64_t seed, int64_t count, int32_t k, int32_t *d_owner, cudaStream_t s);
-
-scd_status setup_owner(scd_ctx *c);  // owner-computes layout (layout.cu), after build_schedule's binning
-int owner_warps();                    // warps per owner CTA (epoch.cu)
-int owner_lag();                      // units between a warp's gather-dot of a unit and its scatter (epoch.cu)
-int owner_hot();                      // an owner's hottest local features, combined per warp (epoch.cu)
 
 // hot.cu ---------------------------------------------------------------------------------------
 scd_status setup_hot(scd_ctx *c);

@@ -829,236 +829,6 @@ __global__ void __launch_bounds__(G *T, 1) k_epoch_sm_tma(EpochArgs a, BinArgs b
 }
 
 // ----------------------------------------------------------------------------------------------
-// Owner-computes dual epoch (default for the single-bin dual when w̄'s active extent fits the SMs'
-// shared memory: C3; DESIGN.md §6 "Owner-computes dual kernel", reading c33).
-//
-// w̄ is partitioned over P CTAs, one per SM: feature j is owned by CTA j mod P at local index j / P, and
-// the owner keeps its part of w̄ in shared memory for the whole epoch (C3: 4 600 floats per CTA).  The
-// entries of every row are regrouped by owner at create (layout.cu setup_owner), so owner k streams,
-// for every row, only the row's entries it owns (~25 of C3's 3 728).  Every owner visits all rows in
-// the same epoch order (block order, reading c28), 32 rows per unit, its W warps taking units in turn:
-//   gather-dot: lane i computes row i's partial dot over the owner's entries from shared memory, adds
-//     it to part[t] (one RED per row) and counts its arrival in cnt[t]; the owner that arrives last
-//     has the whole dot: it computes the closed-form delta (Eq. 4), writes α and publishes dlt[t];
-//   scatter (one unit later, the warp's previous unit): once dlt[t] is published the warp applies
-//     every row's owned entries to its shared-memory w̄ (lanes = a row's entries: unique features),
-//     shared-memory atomic adds (the owner's warps may hit the same feature).
-// No gather or reduction of w̄ goes through L2; per row and owner there is one RED, one counter atomic
-// and one delta read.  A row's dot misses, in each owner's part of w̄, the rows that owner has in flight
-// (two units per warp) and the spread between the owners (bounded by the same window: a warp cannot
-// scatter before every owner has passed its unit): reading c33.  Every owner's dot of unit u precedes
-// its wait for unit u - 1 in program order, so the waits cannot deadlock while all P CTAs are resident
-// (cooperative launch); a spin that runs too long raises own_err instead of hanging.
-struct OwnArgs {
-  const int64_t *offs;  // [P][n + 1]
-  const int32_t *lidx;  // local feature index of every regrouped entry
-  const float *lval;    // its value (nullptr: implicit 1)
-  float *part;          // [positions]: partial dots
-  unsigned *cnt;        // [positions]: owners arrived
-  float *dlt;           // [positions]: published deltas (NaN = not yet)
-  int *err;
-  int64_t n, nsh;       // rows, shared-vector length
-  int P, L;             // owners, local features per owner
-};
-
-__device__ __forceinline__ float ld_volatile_f32(const float *p) {
-  float v;
-  asm volatile("ld.volatile.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_volatile_f32(float *p, float v) {
-  asm volatile("st.volatile.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
-constexpr int kOwnLag = 1;  // units between a warp's gather-dot of a unit and its scatter
-constexpr int kOwnHot = 64; // an owner's hottest local features, combined per warp in the scatter
-
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned *p, unsigned v) {
-  unsigned r;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
-  return r;
-}
-__device__ __forceinline__ void st_release_f32(float *p, float v) {
-  asm volatile("st.release.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-__device__ __forceinline__ float ld_relaxed_f32(const float *p) {
-  float v;
-  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Prefetch the regrouped entries [s0, s1) into L2 (no shared memory): the gather-dot's loads then hit L2.
-__device__ __forceinline__ void own_prefetch(const OwnArgs &o, int64_t s0, int64_t s1, int64_t tot4) {
-  const int64_t a0 = s0 & ~(int64_t)3;
-  const int64_t a1 = min((s1 + 3) & ~(int64_t)3, tot4);
-  if (a1 <= a0) return;
-  const unsigned bytes = (unsigned)(a1 - a0) * 4u;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(o.lidx + a0), "r"(bytes) : "memory");
-  if (o.lval) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(o.lval + a0), "r"(bytes) : "memory");
-}
-
-template <int FORM>
-__global__ void __launch_bounds__(1024, 1) k_epoch_owner(EpochArgs a, BinArgs b, OwnArgs o) {
-  extern __shared__ float s_ow[];
-  const unsigned FULL = 0xffffffffu;
-  const int k = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
-  float *hp = s_ow + w * kOwnHot;  // this warp's pending updates of the owner's hottest features
-  float *Wv = s_ow + W * kOwnHot;  // the owner's part of w̄
-  for (int l = lane; l < kOwnHot; l += 32) hp[l] = 0.f;
-  for (int l = threadIdx.x; l < o.L; l += blockDim.x) {
-    const int64_t g = k + (int64_t)o.P * l;
-    Wv[l] = g < o.nsh ? __ldcg(a.sv + g) : 0.f;
-  }
-  __syncthreads();
-  const int64_t *offk = o.offs + (int64_t)k * (o.n + 1);
-  const int64_t tot4 = (o.offs[(int64_t)o.P * (o.n + 1) - 1]) & ~(int64_t)3;
-  const int64_t npos = b.hi - b.lo;
-  const int64_t nunits = (npos + 31) / 32;
-  // this lane's row of a unit: coordinate, owned-entry range, and (for the last owner to arrive) its
-  // model value, norm and label, loaded a unit ahead
-  struct Row {
-    int64_t c, o0, o1;
-    float x, nrm, y;
-  };
-  auto row_of = [&](int64_t u, Row &r) {
-    const int64_t tp = u * 32 + lane;
-    r.c = -1;
-    r.o0 = r.o1 = 0;
-    r.x = r.nrm = r.y = 0.f;
-    if (u < nunits && tp < npos) {
-      r.c = bin_coord(b, b.lo + tp);
-      r.o0 = __ldg(offk + r.c);
-      r.o1 = __ldg(offk + r.c + 1);
-      r.x = a.x[r.c];
-      r.nrm = __ldg(a.norm + r.c);
-      r.y = FORM == SCD_DUAL ? __ldg(a.y + r.c) : 0.f;
-    }
-  };
-  // the unit's rows are consecutive coordinates of the bin (block order; all non-empty rows are in the
-  // bin), so their owned entries form one contiguous span: prefetched into L2 a unit ahead
-  auto prefetch_unit = [&](const Row &r) {
-    const unsigned vm = __ballot_sync(FULL, r.c >= 0);
-    if (vm == 0) return;
-    const int64_t s0 = __shfl_sync(FULL, r.o0, 0), s1 = __shfl_sync(FULL, r.o1, 31 - __clz(vm));
-    if (lane == 0) own_prefetch(o, s0, s1, tot4);
-  };
-  Row cur, nxt;
-  row_of(w, cur);
-  prefetch_unit(cur);
-  row_of(w + W, nxt);
-  prefetch_unit(nxt);
-  bool pv = false;  // the pending unit (kOwnLag = 1): this lane's row
-  int64_t pt = 0, p0 = 0, p1 = 0;
-  for (int64_t u = w;; u += W) {
-    const bool have = u < nunits;
-    const int64_t tp = u * 32 + lane;
-    Row nn;
-    row_of(u + 2 * (int64_t)W, nn);
-    // gather-dot of this lane's row (its entries read through L1, four in flight)
-    float p = 0.f;
-    for (int64_t e = cur.o0; e < cur.o1; e += 8) {
-      int32_t j[8];
-      float v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const bool in = e + q < cur.o1;
-        j[q] = in ? __ldg(o.lidx + e + q) : 0;
-        v[q] = in ? (o.lval ? __ldg(o.lval + e + q) : 1.f) : 0.f;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) p = fmaf(Wv[j[q]], v[q], p);
-    }
-    if (cur.c >= 0) {
-      if (p != 0.f) atomicAdd(o.part + tp, p);
-      // the arrival is counted after the partial (release); the last owner sees every partial (acquire)
-      if (atom_add_acq_rel(o.cnt + tp, 1u) == (unsigned)o.P - 1u) {
-        const float sum = __ldcg(o.part + tp);
-        const float d = coord_delta<FORM>(sum, cur.x, cur.nrm, cur.y, a.lam, a.lamN);
-        if (!b.dry) a.x[cur.c] = cur.x + d;  // single writer per epoch (c10)
-        st_release_f32(o.dlt + tp, b.dry ? 0.f : d);
-      }
-    }
-    // scatter of the pending unit once its deltas are published, row by row with lanes = the row's entries
-    // (distinct features); the owner's hottest features (local index < kOwnHot: the head of w̄, carried by
-    // most rows) are summed in the warp's private pending array and added to w̄ once per unit, the rest
-    // with shared-memory atomic adds (the owner's warps rarely hit the same feature at the same time)
-    if (__any_sync(FULL, pv)) {
-      float x = 0.f;
-      if (pv) {
-        unsigned spins = 0;
-        while (isnan(x = ld_relaxed_f32(o.dlt + pt))) {
-          // ~0.3 s: a lost arrival; report instead of hanging (and stop waiting anywhere once reported)
-          if (++spins > (1u << 22) || (spins % 1024 == 0 && *(volatile int *)o.err)) {
-            atomicExch(o.err, 1);
-            x = 0.f;
-            break;
-          }
-          __nanosleep(32);
-        }
-      }
-      const float dme = scatter_scale<FORM>(x);
-      // four rows at a time: their loads are in flight together
-      for (int i0 = 0; i0 < 32; i0 += 4) {
-        float d[4];
-        int64_t r0[4], r1[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          d[q] = __shfl_sync(FULL, dme, i0 + q);
-          r0[q] = __shfl_sync(FULL, p0, i0 + q);
-          r1[q] = __shfl_sync(FULL, p1, i0 + q);
-        }
-        int64_t mx = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) mx = max(mx, r1[q] - r0[q]);
-        for (int64_t off0 = 0; off0 < mx; off0 += 32) {  // warp-uniform trip count
-          const int64_t off = off0 + lane;
-          int32_t j[4];
-          float v[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const bool in = d[q] != 0.f && r0[q] + off < r1[q];
-            j[q] = in ? __ldg(o.lidx + r0[q] + off) : -1;
-            v[q] = in ? (o.lval ? __ldg(o.lval + r0[q] + off) : 1.f) * d[q] : 0.f;
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {  // rows one after another: distinct features within each row
-            if (j[q] >= kOwnHot)
-              atomicAdd(&Wv[j[q]], v[q]);
-            else if (j[q] >= 0)
-              hp[j[q]] += v[q];
-            __syncwarp();
-          }
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int q = 0; q < kOwnHot / 32; ++q) {
-        const int l = q * 32 + lane;
-        const float v = hp[l];
-        if (v != 0.f) {
-          atomicAdd(&Wv[l], v);
-          hp[l] = 0.f;
-        }
-      }
-      __syncwarp();
-    }
-    if (!have) break;
-    pv = cur.c >= 0;
-    pt = tp;
-    p0 = cur.o0;
-    p1 = cur.o1;
-    cur = nxt;
-    nxt = nn;
-    prefetch_unit(nxt);
-  }
-  __syncthreads();  // every warp has applied its last unit
-  for (int l = threadIdx.x; l < o.L; l += blockDim.x) {
-    const int64_t g = k + (int64_t)o.P * l;
-    if (g < o.nsh) a.sv[g] = Wv[l];
-  }
-}
-
-// ----------------------------------------------------------------------------------------------
 template <int FORM, int G, int E, bool WILD = false>
 __global__ void __launch_bounds__(256) k_epoch_group(EpochArgs a, BinArgs b) {
   constexpr int CPW = 32 / G;  // coordinates per warp per ticket
@@ -2073,75 +1843,6 @@ bool sm_head_shape(scd_ctx *c, Bin &b) {
 int sm_chunk_entries() { return kSmC; }
 
 // warps per owner CTA of k_epoch_owner (SCD_OWNER_W overrides, 1..16)
-int owner_lag() { return kOwnLag; }
-int owner_hot() { return kOwnHot; }
-int owner_warps() {
-  int w = 32;
-  if (const char *e = getenv("SCD_OWNER_W")) w = atoi(e);
-  return std::max(1, std::min(32, w));
-}
-
-// One owner-computes launch over the positions [lo, hi) of the single bin (run_epoch).
-static scd_status run_owner(scd_ctx *c, uint32_t epoch, int part, int nparts) {
-  Bin &b = c->bins[0];
-  cudaStream_t s = c->stream;
-  EpochArgs a = make_args(c);
-  BinArgs ba;
-  ba.list = b.list;
-  ba.lo = b.count * part / nparts;
-  ba.hi = b.count * (part + 1) / nparts;
-  if (ba.hi <= ba.lo) return SCD_OK;
-  ba.counter = c->counters;
-  ba.blk = b.blk;
-  ba.blk_shift = b.blk_shift;
-  ba.bperm = nullptr;
-  ba.zero = 0;
-  ba.dry = 0;
-  ba.perm = make_perm(c->opt.seed, epoch, b.stream_id, b.blk > 1 ? b.count / b.blk : b.count);
-  if (b.blk > 1 && b.bperm && ba.perm.n > 0) {
-    if (part == 0 || nparts == 1) {
-      k_block_perm<<<grid_for((int64_t)ba.perm.n, 256), 256, 0, s>>>(ba.perm, (int64_t)ba.perm.n, b.bperm);
-      SCD_CKL(c, "k_block_perm launch");
-      ++c->launches;
-    }
-    ba.bperm = b.bperm;
-  }
-  const int64_t np = ba.hi - ba.lo;
-  SCD_CK(c, cudaMemsetAsync(c->own_part, 0, sizeof(float) * (size_t)np, s));
-  SCD_CK(c, cudaMemsetAsync(c->own_cnt, 0, sizeof(unsigned) * (size_t)np, s));
-  SCD_CK(c, cudaMemsetAsync(c->own_dlt, 0xff, sizeof(float) * (size_t)np, s));  // NaN: not yet published
-  OwnArgs o;
-  o.offs = c->own_offs;
-  o.lidx = c->own_lidx;
-  o.lval = c->own_lval;
-  o.part = c->own_part;
-  o.cnt = c->own_cnt;
-  o.dlt = c->own_dlt;
-  o.err = c->own_err;
-  o.n = c->n_coord;
-  o.nsh = c->n_shared;
-  o.P = c->own;
-  o.L = c->own_L;
-  void *fn = c->form == SCD_PRIMAL ? (void *)k_epoch_owner<SCD_PRIMAL> : (void *)k_epoch_owner<SCD_DUAL>;
-  const size_t smem = sizeof(float) * ((size_t)c->own_L + (size_t)owner_hot() * c->own_w);
-  if (smem >= 48 * 1024) SCD_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  void *args[] = {&a, &ba, &o};
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c->opt.profile) {
-    e0 = get_event(c);
-    e1 = get_event(c);
-    cudaEventRecord(e0, s);
-  }
-  // cooperative: every owner CTA must be resident (they wait on each other's partial sums)
-  SCD_CK(c, cudaLaunchCooperativeKernel(fn, dim3((unsigned)c->own), dim3(32 * c->own_w), args, smem, s));
-  ++c->launches;
-  if (c->opt.profile) {
-    cudaEventRecord(e1, s);
-    c->ev_pending.push_back({0, {e0, e1}});
-  }
-  return SCD_OK;
-}
-
 // Launch one bin's kernel over the permutation positions [ba.lo, ba.hi) with `grid` CTAs.
 scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64_t grid, cudaStream_t s) {
   void *fn = bin_kernel(c, b);
@@ -2195,7 +1896,6 @@ scd_status run_epoch(scd_ctx *c, uint32_t epoch, int part, int nparts) {
   }
   c->empty_dirty = false;
   if (c->n_bins == 0) return SCD_OK;
-  if (c->own) return run_owner(c, epoch, part, nparts);
   // The epoch visits each bin in its own random order; the bins are interleaved in S slices so
   // that, at the granularity of a slice, the epoch order stays a random mix of all coordinates
   // (a bin-by-bin order converges much more slowly, DESIGN.md §6 / reading c24).

@@ -675,118 +675,6 @@ scd_status build_schedule(scd_ctx *c) {
   }
   // one ticket counter per (slice, bin)
   SCD_CK(c, cudaMalloc((void **)&c->counters, sizeof(unsigned int) * kMaxBins * kMaxSlices));
-  return setup_owner(c);
-}
-
-// ----------------------------------------------------------------------------------------------
-// Owner-computes layout for the dual (DESIGN.md §6 "Owner-computes dual kernel"): feature j is owned by
-// CTA j mod P (P = SMs, one CTA each) at local index j / P; the entries of every row are regrouped by
-// owner: for owner k, the rows in storage order, each row's entries owned by k (local index, value).
-// own_offs[k * (N + 1) + n] = global position of the first such entry of row n (an exclusive scan of the
-// per-(owner, row) counts), so row n's entries of owner k are [own_offs[k][n], own_offs[k][n + 1]).
-__global__ void k_own_count(const int64_t *ptr, const int32_t *idx, int64_t n, int P, int64_t *cnt) {
-  extern __shared__ int s_h[];  // [warps][P]
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  int *h = s_h + wl * P;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
-    for (int k = lane; k < P; k += 32) h[k] = 0;
-    __syncwarp();
-    for (int64_t e = ptr[r] + lane; e < ptr[r + 1]; e += 32) atomicAdd(&h[idx[e] % P], 1);
-    __syncwarp();
-    for (int k = lane; k < P; k += 32) cnt[(int64_t)k * (n + 1) + r] = h[k];
-    __syncwarp();
-  }
-}
-
-__global__ void k_own_scatter(const int64_t *ptr, const int32_t *idx, const float *val, int64_t n, int P,
-                              const int64_t *offs, int32_t *lidx, float *lval) {
-  extern __shared__ int s_h[];  // [warps][P] cursors relative to the row's start in each owner
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  int *h = s_h + wl * P;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
-    for (int k = lane; k < P; k += 32) h[k] = 0;
-    __syncwarp();
-    for (int64_t e = ptr[r] + lane; e < ptr[r + 1]; e += 32) {
-      const int32_t j = idx[e];
-      const int k = j % P;
-      const int64_t pos = offs[(int64_t)k * (n + 1) + r] + atomicAdd(&h[k], 1);
-      lidx[pos] = j / P;
-      if (lval) lval[pos] = val[e];
-    }
-    __syncwarp();
-  }
-}
-
-// Eligibility: the dual with one asynchronous bin of CTA (or longer) coordinates, w̄'s active extent
-// fitting the owners' shared memory, and the kernel's rows in flight ((lag + 2) · 32 · warps: each warp
-// has its current unit and `lag` units awaiting their scatter, plus one unit for the owners' spread,
-// DESIGN.md reading c33) within the bin's cap and 1/8 of the bin.  SCD_OWNER=0 disables it.
-scd_status setup_owner(scd_ctx *c) {
-  c->own = 0;
-  const char *e = getenv("SCD_OWNER");  // opt-in experiment (measured slower than k_epoch_sm_tma on C3)
-  if (!(e && atoi(e) == 1) || c->form != SCD_DUAL || c->opt.deterministic || c->opt.wild || c->opt.max_inflight > 0 ||
-      c->n_bins != 1 || c->bins[0].lanes < kLanesCta || c->nnz == 0 || c->n_coord > INT32_MAX)
-    return SCD_OK;
-  Bin &B = c->bins[0];
-  const int P = c->nsm;
-  const int64_t L = (c->sv_active + P - 1) / P;
-  if (L * 4 > 200 * 1024) return SCD_OK;
-  // warps per owner: as many as the in-flight budget allows (at most owner_warps())
-  const double budget = std::min<double>((double)B.cap, (double)B.count / 8.0);
-  const int W = std::min(owner_warps(), (int)(budget / ((owner_lag() + 2) * 32.0)));
-  if (W < 4) return SCD_OK;
-  const int64_t n = c->n_coord;
-  cudaStream_t s = c->stream;
-  const size_t nofs = (size_t)P * (size_t)(n + 1);
-  auto bail = [&](const char *what) {
-    cudaGetLastError();
-    cudaFree(c->own_offs);
-    cudaFree(c->own_lidx);
-    cudaFree(c->own_lval);
-    c->own_offs = nullptr;
-    c->own_lidx = nullptr;
-    c->own_lval = nullptr;
-    (void)what;
-    return SCD_OK;  // not enough memory for the regrouped copy: keep the other kernels
-  };
-  if (cudaMalloc((void **)&c->own_offs, sizeof(int64_t) * nofs) != cudaSuccess) return bail("offs");
-  if (cudaMalloc((void **)&c->own_lidx, sizeof(int32_t) * (size_t)c->nnz) != cudaSuccess) return bail("lidx");
-  if (c->val && cudaMalloc((void **)&c->own_lval, sizeof(float) * (size_t)c->nnz) != cudaSuccess) return bail("lval");
-  const int T = 256;
-  const size_t sh = sizeof(int) * (size_t)(T / 32) * P;
-  k_own_count<<<grid_for(n * 32, T, 148 * 16), T, sh, s>>>(c->ptr, c->idx, n, P, c->own_offs);
-  SCD_CKL(c, "k_own_count");
-  void *tmp = nullptr;
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, c->own_offs, c->own_offs, (int64_t)nofs, s);
-  SCD_CK(c, cudaMallocAsync(&tmp, tb, s));
-  SCD_CK(c, cub::DeviceScan::ExclusiveSum(tmp, tb, c->own_offs, c->own_offs, (int64_t)nofs, s));
-  cudaFreeAsync(tmp, s);
-  k_own_scatter<<<grid_for(n * 32, T, 148 * 16), T, sh, s>>>(c->ptr, c->idx, c->val, n, P, c->own_offs, c->own_lidx,
-                                                            c->own_lval);
-  SCD_CKL(c, "k_own_scatter");
-  SCD_CK(c, cudaMalloc((void **)&c->own_part, sizeof(float) * (size_t)std::max<int64_t>(n, 1)));
-  SCD_CK(c, cudaMalloc((void **)&c->own_cnt, sizeof(unsigned) * (size_t)std::max<int64_t>(n, 1)));
-  SCD_CK(c, cudaMalloc((void **)&c->own_dlt, sizeof(float) * (size_t)std::max<int64_t>(n, 1)));
-  SCD_CK(c, cudaMalloc((void **)&c->own_err, sizeof(int)));
-  SCD_CK(c, cudaMemsetAsync(c->own_err, 0, sizeof(int), s));
-  // block order of the rows (reading c28): a 32-row unit of the kernel is 32 consecutive rows, so its
-  // offsets and entries are contiguous in every owner's regrouped layout
-  if (B.blk != 32) {
-    cudaFree(B.bperm);
-    B.bperm = nullptr;
-    B.blk = 32;
-    B.blk_shift = 5;
-    if (B.count / 32 > 0) SCD_CK(c, cudaMalloc((void **)&B.bperm, sizeof(int32_t) * (size_t)(B.count / 32)));
-  }
-  SCD_CK(c, cudaStreamSynchronize(s));
-  c->own = P;
-  c->own_L = (int)L;
-  c->own_w = W;
-  B.grid = P;
-  B.block = 32 * W;
   return SCD_OK;
 }
 

@@ -62,8 +62,7 @@ class Info(C.Structure):
                 ("sv_offset_bytes", C.c_int64), ("probe_best_ms", C.c_float), ("probe_worst_ms", C.c_float),
                 ("bin_head", C.c_int32 * 4), ("bin_flush", C.c_int32 * 4), ("bin_hot", C.c_int32 * 4),
                 ("hot_cover", C.c_double), ("tail_snap", C.c_int32), ("tail_tau", C.c_double), ("bin_snap", C.c_int32 * 4), ("tail_roll", C.c_int64), ("head_copy", C.c_int64), ("hot_copy", C.c_int64), ("hot_tp", C.c_int32), ("hot_tail_tau", C.c_double), ("hot_hp", C.c_int32),
-                ("sm_head", C.c_int32), ("sm_chunk", C.c_int32), ("sm_ch", C.c_int32), ("sm_rh", C.c_int32),
-                ("own", C.c_int32), ("own_warps", C.c_int32), ("own_err", C.c_int32)]
+                ("sm_head", C.c_int32), ("sm_chunk", C.c_int32), ("sm_ch", C.c_int32), ("sm_rh", C.c_int32)]
 
 
 _lib = None
@@ -256,7 +255,6 @@ class Solver:
                     probe_ms=(inf.probe_best_ms, inf.probe_worst_ms), hot_cover=inf.hot_cover, tail_snap=inf.tail_snap,
                     tail_tau=inf.tail_tau, tail_roll=inf.tail_roll, head_copy=inf.head_copy, hot_copy=inf.hot_copy, hot_tp=inf.hot_tp, hot_tail_tau=inf.hot_tail_tau, hot_hp=inf.hot_hp,
                     sm_head=inf.sm_head, sm_chunk=inf.sm_chunk, sm_ch=inf.sm_ch, sm_rh=inf.sm_rh,
-                    own=inf.own, own_warps=inf.own_warps, own_err=inf.own_err,
                     bins=[dict(lanes=inf.bin_kind[i], count=inf.bin_count[i], nnz=inf.bin_nnz[i],
                                grid=inf.bin_grid[i], block=inf.bin_block[i], cap=inf.bin_cap[i],
                                tau=inf.bin_tau[i], head=inf.bin_head[i], flush=inf.bin_flush[i],

@@ -39,7 +39,7 @@ def child(which, E):
     info = s.info()
     s.close()
     print("RESULT " + json.dumps(dict(rows=out, bins=info["bins"], n_slices=info["n_slices"],
-                                      sm={k: info.get(k) for k in ("own", "own_warps", "own_err", "sm_head", "tail_roll")})))
+                                      sm={k: info.get(k) for k in ("sm_head", "sm_ch", "sm_rh", "tail_roll", "head_copy")})))
 
 
 def main():
