@@ -64,25 +64,76 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML in a background
+    thread every 10 ms (a sample on entry and one on exit, so even a 150 ms region has ~15); falls back to
+    `nvidia-smi -lms` when NVML is unavailable."""
+
+    _REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.sm, self.mx, self.reasons = [], 0.0, set()
+        self.stop = None
+        self.th = None
+        self.nv = None
+        self.f = None
         self.p = None
 
-    def __enter__(self):
+    def _sample(self):
+        nv, h = self.nv, self.h
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        self.mx = max(self.mx, float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
         except Exception:
-            self.p = None
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        for n, bit in self._REASONS.items():
+            if r & bit:
+                self.reasons.add(n)
+
+    def __enter__(self):
+        import threading
+
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[self.gpu].isdigit() else self.gpu
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(idx)
+            self._sample()
+            self.stop = threading.Event()
+
+            def loop():
+                while not self.stop.wait(0.01):
+                    try:
+                        self._sample()
+                    except Exception:
+                        return
+
+            self.th = threading.Thread(target=loop, daemon=True)
+            self.th.start()
+        except Exception:
+            self.nv = None
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            try:
+                self.p = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+            except Exception:
+                self.p = None
         return self
 
     def __exit__(self, *a):
+        if self.nv is not None:
+            self.stop.set()
+            self.th.join(timeout=2)
+            try:
+                self._sample()
+            except Exception:
+                pass
         if self.p:
             self.p.terminate()
             try:
@@ -91,25 +142,26 @@ class ClockSampler:
                 self.p.kill()
 
     def summary(self):
-        self.f.flush()
-        self.f.seek(0)
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+        if self.nv is None and self.f is not None:
+            self.f.flush()
+            self.f.seek(0)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in self.f.read().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx = max(self.mx, float(parts[1]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        self.reasons.add(n)
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 def c3_cfg(world: int):
