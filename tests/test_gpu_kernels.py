@@ -297,3 +297,28 @@ def test_schedule_rules_small_lambda():
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"])
     assert gaps[-1] <= 1e-5
     check_stress_band(gaps, *env, label="small lambda")
+
+
+def test_sm_head_kernel_implicit_values(c3p, monkeypatch):
+    """The SM-shared head kernel with val = NULL (NEXT-1: the bulk copies then move indices only): the C3
+    prefix's pattern with every value 1, against the oracle solving the same problem with explicit ones."""
+    monkeypatch.delenv("SCD_HEAD", raising=False)
+    monkeypatch.delenv("SCD_SM_HEAD", raising=False)
+    d, _, _, _ = c3p
+    ones = dict(d)
+    ones["val"] = np.ones_like(d["val"])
+    pr = solver.Problem.from_csr(ones, lam=1e-3 * 350_000 / 20_000)
+    _, _, hist = solver.solve(pr, "dual", 8, seed=4)
+    s = scd.Solver(d["ptr"], d["idx"], None, pr.N, pr.M, d["y"], pr.lam, "dual", seed=4)
+    info = s.info()
+    gaps = []
+    for t in range(1, 9):
+        s.epoch(t)
+        gaps.append(s.duality_gap())
+    x = s.get_model().astype(np.float64)
+    s.close()
+    A = pr.A()
+    Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+    print("implicit sm head", info["sm_head"], ["%.2e" % g for g in gaps], ["%.2e" % h["gap"] for h in hist])
+    assert info["sm_head"] == 4, info
+    assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"]) and gaps[-1] <= 1e-5, (Pg, hist[-1]["P"], gaps)
