@@ -304,10 +304,14 @@ def test_sm_head_kernel_implicit_values(c3p, monkeypatch):
     prefix's pattern with every value 1, against the oracle solving the same problem with explicit ones."""
     monkeypatch.delenv("SCD_HEAD", raising=False)
     monkeypatch.delenv("SCD_SM_HEAD", raising=False)
-    d, _, _, _ = c3p
+    d, pr0, _, _ = c3p
     ones = dict(d)
     ones["val"] = np.ones_like(d["val"])
-    pr = solver.Problem.from_csr(ones, lam=1e-3 * 350_000 / 20_000)
+    # λ scaled by the ratio of the squared row norms so that λN / ||a||² (the conditioning, hence the
+    # staleness bound and the launch shape) is that of the C3 prefix with its values
+    lens = np.diff(d["ptr"]).astype(np.float64)
+    nrm = np.add.reduceat(d["val"].astype(np.float64) ** 2, d["ptr"][:-1])
+    pr = solver.Problem.from_csr(ones, lam=pr0.lam * lens.mean() / nrm.mean())
     _, _, hist = solver.solve(pr, "dual", 8, seed=4)
     s = scd.Solver(d["ptr"], d["idx"], None, pr.N, pr.M, d["y"], pr.lam, "dual", seed=4)
     info = s.info()
