@@ -326,3 +326,26 @@ def test_sm_head_kernel_implicit_values(c3p, monkeypatch):
     print("implicit sm head", info["sm_head"], ["%.2e" % g for g in gaps], ["%.2e" % h["gap"] for h in hist])
     assert info["sm_head"] == 4, info
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"]) and gaps[-1] <= 1e-5, (Pg, hist[-1]["P"], gaps)
+
+
+def test_sm_head_kernel_sub_epoch_parts(c3p, monkeypatch):
+    """scd_epoch_part (sub-epoch rounds) through the SM-shared head kernel: each epoch as 4
+    parts (ticket ranges of the same permutation, the rolling tail copy keyed by the global position)
+    reaches the oracle's optimum like whole epochs."""
+    monkeypatch.delenv("SCD_HEAD", raising=False)
+    monkeypatch.delenv("SCD_SM_HEAD", raising=False)
+    d, pr, hist, _ = c3p
+    s = scd.Solver(d["ptr"], d["idx"], d["val"], pr.N, pr.M, d["y"], pr.lam, "dual", seed=4)
+    assert s.info()["sm_head"] == 4
+    gaps = []
+    for t in range(1, E + 1):
+        for p in range(4):
+            s.epoch_part(t, p, 4)
+        gaps.append(s.duality_gap())
+    x = s.get_model().astype(np.float64)
+    s.close()
+    A = pr.A()
+    Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+    print("parts gaps", ["%.2e" % g for g in gaps])
+    assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"]) and gaps[-1] <= 1e-5, (Pg, gaps)
+    assert gaps[2] <= 4 * hist[2]["gap"], (gaps[2], hist[2]["gap"])  # per-epoch rate kept (loose: 4x)
