@@ -533,7 +533,7 @@ scd_status scd_get_info(scd_ctx *c, scd_info *info) {
   for (int i = 0; i < c->n_bins && i < 4; ++i)
     if (c->bins[i].sm) {
       info->sm_head = c->bins[i].sm;
-      info->sm_chunk = sm_chunk_entries();
+      info->sm_chunk = sm_chunk_entries(c->bins[i].sm);
       info->sm_ch = c->bins[i].sm_ch;
       info->sm_rh = c->bins[i].sm_rh;
     }

@@ -241,7 +241,7 @@ scd_status tune_shared_layout(scd_ctx *c);
 void bin_launch_shape(scd_ctx *c, Bin &b);
 double combine_budget(const scd_ctx *c, const Bin &b);  // deferred-update budget of a bin (reading c25)
 bool sm_head_shape(scd_ctx *c, Bin &b);  // SM-shared head kernel shape (false = not used)
-int sm_chunk_entries();                  // SM-shared head kernel: entries per staged chunk
+int sm_chunk_entries(int groups);        // SM-shared head kernel: entries per staged chunk
 double cap_fraction();  // in-flight cap as a fraction of a staleness bound (layout.cu)
 scd_status launch_perm_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t *d_out, cudaStream_t s);
 scd_status launch_block_order_export(uint64_t seed, uint32_t epoch, uint32_t stream, int64_t n, int64_t blk,

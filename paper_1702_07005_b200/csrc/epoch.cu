@@ -1519,7 +1519,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T) k_epoch_cluster_
 
 // kernel table ---------------------------------------------------------------------------------
 constexpr int kCtaT = kLanesCta, kCtaE = 16;
-constexpr int kSmG = 4, kSmC = 2048;  // SM-shared head kernel: row groups per SM, entries per staged chunk
+// SM-shared head kernel (default shape): row groups per SM, threads per group, entries per staged chunk.
+// 6 x 128 x 1024: 6.99 ms per C3 epoch; 4 x 256 x 2048 (SCD_SM_GRP=4): 7.7 ms, with a per-epoch rate
+// ~20% better at tight gaps; 8 x 128 x 1024 (SCD_SM_GRP=8): 6.99 ms (profiles/r2/sm_groups_r2.txt)
+constexpr int kSmG = 6, kSmT = 128, kSmC = 1024;
 constexpr int kGrpE8 = 8, kGrpE32 = 16;
 constexpr int kClE = 8;
 constexpr int kCombT = 128, kCombS = 2048;  // CTA-combining kernel for 8-lane bins
@@ -1596,7 +1599,8 @@ void *bin_kernel(const scd_ctx *c, const Bin &b) {
   }
   if (c->opt.wild) return c->form == SCD_PRIMAL ? kernel_wild<SCD_PRIMAL>(b.lanes) : kernel_wild<SCD_DUAL>(b.lanes);
   if (b.head > 0 && b.lanes == kLanesCta && b.sm && c->form == SCD_DUAL && c->tail_snap)
-    return (void *)k_epoch_sm_tma<SCD_DUAL, kSmG, kCtaT, kSmC>;
+    return b.sm == 4 ? (void *)k_epoch_sm_tma<SCD_DUAL, 4, 256, 2048>
+                     : (b.sm == 8 ? (void *)k_epoch_sm_tma<SCD_DUAL, 8, kSmT, kSmC> : (void *)k_epoch_sm_tma<SCD_DUAL, kSmG, kSmT, kSmC>);
   if (b.head > 0 && b.lanes == kLanesCta) {
     // the read copies exist only for the dual (setup_tail_snap); the head copy needs the rolling tail copy
     if (c->form == SCD_DUAL && c->tail_snap && c->head_copy > 0)
@@ -1790,13 +1794,14 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
 // Dynamic shared memory of a bin's kernel.
 size_t bin_smem(const scd_ctx *c, const Bin &b) {
   if (b.hot > 0) return 8 * (size_t)b.hot;
-  if (b.head > 0 && b.sm) return 2 * sizeof(float) * (size_t)b.head + kSmG * sizeof(GroupSmem<kSmC, kCtaT / 32>);
+  if (b.head > 0 && b.sm == 4) return 2 * sizeof(float) * (size_t)b.head + 4 * sizeof(GroupSmem<2048, 8>);
+  if (b.head > 0 && b.sm) return 2 * sizeof(float) * (size_t)b.head + b.sm * sizeof(GroupSmem<kSmC, kSmT / 32>);
   if (b.head > 0) return sizeof(float) * (size_t)b.head;
   return b.lanes == kLanesCluster ? cluster_smem(c) : 0;
 }
 
 // SM-shared head kernel (k_epoch_sm_tma) for the single head bin of a dual with the rolling tail copy
-// (build_schedule): one CTA of kSmG row groups per SM.  Its head staleness (reading c25): rows in flight
+// (build_schedule): one CTA of G row groups per SM (kSmG by default, SCD_SM_GRP = 4 | 8).  Its head staleness (reading c25): rows in flight
 // (nsm·G) + 2·nsm·Q (the other SMs' pending head and what they flushed since a chunk's snapshot, Q rows
 // of each, Q = nh/ch·rh the rows between two refreshes of a chunk) <= the combined-update budget.  ch is
 // the smallest chunk count per flushing row that fits, then rh the largest period (<= 8).  The kernel's
@@ -1806,9 +1811,11 @@ bool sm_head_shape(scd_ctx *c, Bin &b) {
   b.sm = 0;
   const char *e = getenv("SCD_SM_HEAD");
   if ((e && atoi(e) == 0) || b.head <= 0 || b.lanes != kLanesCta || c->form != SCD_DUAL) return false;
-  constexpr int CH = 4 * kCtaT;
+  const int G = getenv("SCD_SM_GRP") ? atoi(getenv("SCD_SM_GRP")) : kSmG, T = G == 4 ? 256 : kSmT;
+  if (G != kSmG && G != 4 && G != 8) return false;
+  const int CH = 4 * T;
   if (b.head % CH != 0) return false;
-  const int64_t inflight = (int64_t)c->nsm * kSmG;
+  const int64_t inflight = (int64_t)c->nsm * G;
   if (b.cap > 0 && inflight > b.cap) return false;
   const double budget = combine_budget(c, b);
   const int nh = b.head / CH;
@@ -1822,25 +1829,32 @@ bool sm_head_shape(scd_ctx *c, Bin &b) {
   if (ch == 0) return false;
   if (ch == 1)
     while (rh < 8 && fits((double)nh * (rh + 1))) ++rh;
-  b.sm = kSmG;
+  if (const char *ec = getenv("SCD_SM_CH")) {  // experiments: more chunks per row (only ever less staleness)
+    const int f = atoi(ec);
+    if (f > ch && f <= nh) {
+      ch = f;
+      rh = 1;
+    }
+  }
+  b.sm = G;
   b.sm_ch = ch;
   b.sm_rh = rh;
   void *fn = bin_kernel(c, b);
   const size_t smem = bin_smem(c, b);
   int occ = 0;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kSmG * kCtaT, smem) != cudaSuccess || occ < 1) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G * T, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
     b.sm = 0;
     return false;
   }
   b.grid = c->nsm;
-  b.block = kSmG * kCtaT;
+  b.block = G * T;
   b.flush = 0;
   return true;
 }
 
-int sm_chunk_entries() { return kSmC; }
+int sm_chunk_entries(int groups) { return groups == 4 ? 2048 : kSmC; }
 
 // warps per owner CTA of k_epoch_owner (SCD_OWNER_W overrides, 1..16)
 // Launch one bin's kernel over the permutation positions [ba.lo, ba.hi) with `grid` CTAs.
