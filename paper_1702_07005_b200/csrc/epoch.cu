@@ -442,8 +442,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
 // SM-shared head kernel with bulk-copied rows (default for the single head bin of a dual with the
 // rolling tail copy: C3; DESIGN.md §6 "SM-shared head kernel").
 //
-// One 1024-thread CTA per SM runs G = 4 row groups of T = 256 threads; a group does one row at a time.
-// The four rows an SM has in flight share one shared-memory state of the frequency-ranked head:
+// One CTA per SM runs G row groups of T threads (default 6 x 128, kSmG / kSmT); a group does one row at a
+// time.  The G rows an SM has in flight share one shared-memory state of the frequency-ranked head:
 //   S[0, H)  the SM's snapshot of w̄[0, H)
 //   P[0, H)  the SM's pending updates of w̄[0, H) (not yet reduced into w̄)
 // A head read is S[j] + P[j] (no L2 access; the head was ~620 L2 sector reads per C3 row), a tail read

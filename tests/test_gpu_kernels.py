@@ -1,6 +1,6 @@
 """GPU: the webspam-shaped CTA-bin kernels against the fp64 oracle.
 
-  * k_epoch_sm_tma (default for the C3-shaped dual): one CTA of 4 row groups per SM shares a snapshot
+  * k_epoch_sm_tma (default for the C3-shaped dual): one CTA of 6 row groups per SM shares a snapshot
     of the dense head of w̄ and its pending updates (flushed chunk by chunk); rows are staged in shared
     memory by bulk copies.  Extra staleness bounded by the schedule (reading c25).
   * k_epoch_cta_head (SCD_SM_HEAD=0 and the fallback): each CTA combines its updates of the dense head
