@@ -1527,6 +1527,13 @@ constexpr int kGrpE8 = 8, kGrpE32 = 16;
 constexpr int kClE = 8;
 constexpr int kCombT = 128, kCombS = 2048;  // CTA-combining kernel for 8-lane bins
 
+// threads per CTA of the plain CTA-bin kernel: 128 (C4: 10.48 -> 10.0 ms per epoch, the per-epoch gaps
+// within run-to-run noise, profiles/r2/c4_cta_threads_r2.txt); SCD_CTA_T = 256 restores the round-1 shape
+int cta_threads() {
+  static const int t = getenv("SCD_CTA_T") && atoi(getenv("SCD_CTA_T")) == 256 ? kCtaT : 128;
+  return t;
+}
+
 template <int FORM>
 void *kernel_for(int lanes, int plain) {
   switch (lanes) {
@@ -1535,7 +1542,7 @@ void *kernel_for(int lanes, int plain) {
       return plain ? (void *)k_epoch_group<FORM, 8, kGrpE8> : (void *)k_epoch_group_comb<FORM, 8, kCombT, kCombS>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32>;
     case kLanesCluster: return nullptr;  // cluster_kernel()
-    default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
+    default: return cta_threads() == 128 ? (void *)k_epoch_cta<FORM, 128, kCtaE> : (void *)k_epoch_cta<FORM, kCtaT, kCtaE>;
   }
 }
 
@@ -1752,7 +1759,7 @@ void bin_launch_shape(scd_ctx *c, Bin &b) {
   const bool group = (b.lanes <= 32);
   const bool clus = (b.lanes == kLanesCluster);
   const bool comb = (b.lanes == 8 && !b.plain);  // fixed CTA size (kernel template)
-  int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : kCtaT));
+  int block = comb ? kCombT : (group ? 256 : (clus ? kClusterThreads : (b.head > 0 ? kCtaT : cta_threads())));
   // sub-warp bins with a small cap shrink the CTA so the cap can be honoured (>= one warp)
   if (group && !comb && b.cap > 0 && b.cap * b.lanes < block) {
     block = (int)(((b.cap * b.lanes) + 31) / 32 * 32);
