@@ -1836,13 +1836,6 @@ bool sm_head_shape(scd_ctx *c, Bin &b) {
   if (ch == 0) return false;
   if (ch == 1)
     while (rh < 8 && fits((double)nh * (rh + 1))) ++rh;
-  if (const char *ec = getenv("SCD_SM_CH")) {  // experiments: more chunks per row (only ever less staleness)
-    const int f = atoi(ec);
-    if (f > ch && f <= nh) {
-      ch = f;
-      rh = 1;
-    }
-  }
   b.sm = G;
   b.sm_ch = ch;
   b.sm_rh = rh;
