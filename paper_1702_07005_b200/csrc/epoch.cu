@@ -168,6 +168,7 @@ __device__ __forceinline__ int64_t bin_coord(const BinArgs &b, uint64_t t) {
 template <int FORM, int T, int E, bool WILD = false>
 __global__ void __launch_bounds__(T) k_epoch_cta(EpochArgs a, BinArgs b) {
   constexpr int NW = T / 32;
+  if (blockDim.x != T) __trap();  // the host's launch shape must match the template
   __shared__ float s_red[NW];
   __shared__ float s_delta;
   __shared__ unsigned int s_ticket;
@@ -277,6 +278,7 @@ __device__ __forceinline__ float ld_entry(const EpochArgs &a, const float *s_acc
 template <int FORM, int T, int E, int TS, bool HC>
 __global__ void __launch_bounds__(T, 1024 / T) k_epoch_cta_head(EpochArgs a, BinArgs b, int H, int flush) {
   constexpr int NW = T / 32;
+  if (blockDim.x != T) __trap();  // the host's launch shape must match the template
   extern __shared__ float4 s_dyn[];
   float *s_acc = reinterpret_cast<float *>(s_dyn);
   __shared__ float s_red[NW];
@@ -669,6 +671,7 @@ __device__ __forceinline__ void chunk_entries(const EpochArgs &a, const GroupSme
 template <int FORM, int G, int T, int C>
 __global__ void __launch_bounds__(G *T, 1) k_epoch_sm_tma(EpochArgs a, BinArgs b, SmHeadArgs h) {
   constexpr int NW = T / 32;
+  if (blockDim.x != G * T) __trap();  // the host's launch shape must match the template
   constexpr int CH = 4 * T;  // floats per flushed chunk (one float4 per thread of a group)
   constexpr int U = C / T;   // entries per thread per chunk
   static_assert(C % T == 0 && U % 4 == 0, "chunk shape");
@@ -1553,7 +1556,7 @@ void *kernel_wild(int lanes) {
     case 8: return (void *)k_epoch_group<FORM, 8, kGrpE8, true>;
     case 32: return (void *)k_epoch_group<FORM, 32, kGrpE32, true>;
     case kLanesCluster: return nullptr;
-    default: return (void *)k_epoch_cta<FORM, kCtaT, kCtaE, true>;
+    default: return cta_threads() == 128 ? (void *)k_epoch_cta<FORM, 128, kCtaE, true> : (void *)k_epoch_cta<FORM, kCtaT, kCtaE, true>;
   }
 }
 
