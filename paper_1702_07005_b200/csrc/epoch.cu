@@ -466,6 +466,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
 // starts with its entries on chip.  A buffer is handed back by the last of the group's warps to read it
 // (shared-memory counter), which issues the next copy into it; the row descriptors and the partial sums
 // are double-buffered by row parity, every warp derives the delta itself: one group barrier per row.
+constexpr int kRollChunk = 1024;  // floats per rolling tail-copy refresh (= 4 * kLanesCta, as build_schedule assumes)
+
 struct SmHeadArgs {
   int H;   // head snapshot / pending extent [0, H), a multiple of 4 * T
   int ch;  // head chunks flushed per flushing row
@@ -748,14 +750,19 @@ __global__ void __launch_bounds__(G *T, 1) k_epoch_sm_tma(EpochArgs a, BinArgs b
       n_tk = ticket_async(b, 1u);
     }
     if (a.roll_R > 0 && !b.dry && r.t % a.roll_R == 0) {
-      // rolling tail copy: row position t refreshes chunk (t / roll_R) mod nchunks of svr
-      const int64_t nch = (a.roll_hi - a.roll_lo + CH - 1) / CH;
-      const int64_t i = a.roll_lo + ((r.t / a.roll_R) % nch) * CH + (int64_t)gt * 4;
+      // rolling tail copy: row position t refreshes chunk (t / roll_R) mod nchunks of svr,
+      // in the 1024-float chunks build_schedule sized roll_R for (kRollChunk), whatever the group size
+      const int64_t nch = (a.roll_hi - a.roll_lo + kRollChunk - 1) / kRollChunk;
       float *dst = const_cast<float *>(a.svr);
-      if (i + 3 < a.roll_hi)
-        *reinterpret_cast<float4 *>(dst + i) = __ldcg(reinterpret_cast<const float4 *>(a.sv + i));
-      else
-        for (int64_t q = i; q < a.roll_hi && q < i + 4; ++q) dst[q] = __ldcg(a.sv + q);
+#pragma unroll
+      for (int q = 0; q < (kRollChunk + 4 * T - 1) / (4 * T); ++q) {
+        const int64_t i = a.roll_lo + ((r.t / a.roll_R) % nch) * kRollChunk + (int64_t)(q * T + gt) * 4;
+        if (q * T + gt >= kRollChunk / 4) break;
+        if (i + 3 < a.roll_hi)
+          *reinterpret_cast<float4 *>(dst + i) = __ldcg(reinterpret_cast<const float4 *>(a.sv + i));
+        else
+          for (int64_t e = i; e < a.roll_hi && e < i + 4; ++e) dst[e] = __ldcg(a.sv + e);
+      }
     }
     // the head chunk this row refreshes: its w̄ value is loaded now, consumed after the gather-dot
     const bool hfl = r.u % (unsigned)h.rh == 0;
