@@ -1690,7 +1690,7 @@ int64_t combine_window(const scd_ctx *c, const Bin &b, int64_t inflight, int64_t
 // window F batches.  At a fixed budget the rows a CTA combines per flush (rows per CTA x F) is what
 // counts: 512 threads at F = 7 beat 256 threads at F = 7 with twice the CTAs (26.9 vs 31.9 ms on a
 // C5 shard).  The grid is lowered (in steps of one CTA per SM, not below one per SM) until F >= 6
-// fits the budget.  SCD_HOT_T=256, SCD_HOT_F, SCD_HOT_CTAS (CTAs per SM) override (experiments).
+// fits the budget.
 void hot_launch_shape(scd_ctx *c, Bin &b) {
   // the 768-thread kernel exists only in the default (hot copy + early gathers) configuration
   // one 512-thread CTA per SM, 64 rows in flight per CTA (profiles/c5_shape_r2.txt: 768 threads are ~5%
@@ -1866,7 +1866,6 @@ bool sm_head_shape(scd_ctx *c, Bin &b) {
 
 int sm_chunk_entries(int groups) { return groups == 4 ? 2048 : kSmC; }
 
-// warps per owner CTA of k_epoch_owner (SCD_OWNER_W overrides, 1..16)
 // Launch one bin's kernel over the permutation positions [ba.lo, ba.hi) with `grid` CTAs.
 scd_status launch_bin(scd_ctx *c, const Bin &b, EpochArgs &a, BinArgs &ba, int64_t grid, cudaStream_t s) {
   void *fn = bin_kernel(c, b);
