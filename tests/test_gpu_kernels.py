@@ -352,3 +352,37 @@ def test_sm_head_kernel_sub_epoch_parts(c3p, monkeypatch):
     # rows in flight are a far larger share than in a full-size part of 87 500, so the per-epoch rate is
     # slower: 5.5e-7 vs 1.3e-7 at epoch 3 with whole epochs)
     assert abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"]) and gaps[-1] <= 1e-5, (Pg, gaps)
+
+
+def test_sm_head_kernel_two_logical_workers(monkeypatch):
+    """Alg. 4 with K = 2 logical workers (the first 40 000 C3 rows split in two 20 000-row blocks, λN = 350
+    as in C3), each running the SM-shared head kernel, optimal γ after every round: the aggregation rewrites
+    w̄ between epochs, so every launch takes its head snapshot and its tail copy afresh.  The global model
+    reaches the oracle's optimum (BASELINE tolerances: gap <= 1e-5, objective within 1e-5)."""
+    monkeypatch.delenv("SCD_HEAD", raising=False)
+    monkeypatch.delenv("SCD_SM_HEAD", raising=False)
+    d = synth.gen_host(synth.CONFIGS["C3"].with_rows(40_000))
+    pr = solver.Problem.from_csr(d, lam=1e-3 * 350_000 / 40_000)
+    _, _, hist = solver.solve(pr, "dual", 12, seed=4)
+    half = pr.N // 2
+    solvers = []
+    for k, (r0, r1) in enumerate(((0, half), (half, pr.N))):
+        p = (d["ptr"][r0:r1 + 1] - d["ptr"][r0]).astype(np.int64)
+        sl = slice(int(d["ptr"][r0]), int(d["ptr"][r1]))
+        solvers.append(scd.Solver(p, d["idx"][sl], d["val"][sl], r1 - r0, pr.M, d["y"][r0:r1], pr.lam, "dual",
+                                  seed=4 + k, n_global=pr.N))
+    infos = [s.info() for s in solvers]
+    assert all(i["sm_head"] > 0 for i in infos), [(i["sm_head"], i["bins"]) for i in infos]
+    gaps = []
+    for t in range(1, 16):
+        for s in solvers:
+            s.epoch(t)
+        scd.aggregate_group(solvers, "optimal")
+        gaps.append(scd.evaluate_group(solvers)[2])
+    x = np.concatenate([s.get_model().astype(np.float64) for s in solvers])
+    for s in solvers:
+        s.close()
+    A = pr.A()
+    Pg = ridge.primal_objective(A, pr.y, pr.lam, ridge.dual_to_primal(A, pr.lam, x))
+    print("K=2 sm head gaps", ["%.2e" % g for g in gaps])
+    assert gaps[-1] <= 1e-5 and abs(Pg - hist[-1]["P"]) <= 1e-5 * abs(hist[-1]["P"]), (gaps, Pg, hist[-1]["P"])
