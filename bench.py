@@ -372,7 +372,7 @@ def kernel_roofline(s, info, kprof, bytes_per_nnz: int, el_ms: float, world: int
         kname = ("k_epoch_sm_tma" if info.get("sm_head") else "k_epoch_cta_head") if bb.get("head") else "k_epoch_cta"
     else:
         kname = "k_epoch_group_hot" if bb.get("hot") else ("k_epoch_group_comb" if bb["lanes"] == 8 else "k_epoch_group")
-    traffic, dram_bytes = None, None
+    traffic, dram_bytes, l2pct = None, None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
@@ -380,6 +380,7 @@ def kernel_roofline(s, info, kprof, bytes_per_nnz: int, el_ms: float, world: int
             rec = tj.get(kname) if isinstance(tj.get(kname), dict) else (tj if (kname + "<") in tj.get("kernel", "") else None)
             if rec:
                 traffic = rec.get("dram_bytes_per_launch")
+                l2pct = rec.get("l2_tag_requests_pct")
         except Exception:
             traffic = None
     out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -389,6 +390,10 @@ def kernel_roofline(s, info, kprof, bytes_per_nnz: int, el_ms: float, world: int
            "kernel": kname, "bin": b_i, "lanes": bb["lanes"], "kernel_ms_avg": ms_b / cnt_b if cnt_b else None,
            "launches_timed": cnt_b, "kernel_share_of_step": ms_b / el_ms if el_ms else None,
            "bytes_per_launch": bytes_launch, "peak_source": peak_src}
+    if l2pct is not None:
+        # the resource that binds the epoch kernels: L2 tag-request throughput of the same
+        # kernel in its ncu --set full capture (profiles/ncu_traffic.json)
+        out["l2_tag_requests_pct_of_peak"] = l2pct
     if traffic and cnt_b:
         # measured DRAM bytes of the same kernel (ncu, per launch) over the same launch time: the shared
         # vector's gathers and REDs mostly hit L2, so this is below the algorithmic rate

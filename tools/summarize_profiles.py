@@ -87,8 +87,10 @@ def ncu(rep, out_prefix, bytes_per_launch=None):
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
         traffic = (tobytes(rd) or 0) + (tobytes(wr) or 0)
+        l2 = r["metrics"].get("lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed")
         js.append(dict(kernel=r["kernel"], dram_bytes_per_launch=traffic,
-                       duration=r["metrics"].get("gpu__time_duration.sum")))
+                       duration=r["metrics"].get("gpu__time_duration.sum"),
+                       l2_tag_requests_pct=float(l2[0].replace(",", "")) if l2 else None))
         if bytes_per_launch:
             md.append(f"Algorithmic bytes per launch (16 B/nnz + 32 B/coord model): {bytes_per_launch:.4g}; "
                       f"measured DRAM traffic per launch: {traffic:.4g} B ({traffic / bytes_per_launch:.2f}x).\n")
@@ -106,7 +108,8 @@ def ncu(rep, out_prefix, bytes_per_launch=None):
         for r in js:
             short = r["kernel"].split("<")[0].split("::")[-1].replace("void ", "").strip()
             cur[short] = dict(source=os.path.basename(out_prefix) + ".json", kernel=r["kernel"],
-                              dram_bytes_per_launch=r["dram_bytes_per_launch"])
+                              dram_bytes_per_launch=r["dram_bytes_per_launch"],
+                              l2_tag_requests_pct=r.get("l2_tag_requests_pct"))
         json.dump(cur, open(tp, "w"), indent=1)
     print("\n".join(md))
 
