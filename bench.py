@@ -12,7 +12,7 @@ atomic scatter; §8(a) rows a1-a6) and, when N > 1, one optimal-gamma aggregatio
 scaling, global N in λN).  The gap evaluation (a7) is off the clock, as in the paper's plots.
 
 Sub-records on the same JSON line:
-  N = 1: "c4_primal" (configs[3] at K = 1: C3's matrix by feature) and "c5_shard" (one GPU's
+  N = 1: "c2" (configs[1], dual and primal), "c4_primal" (configs[3] at K = 1: C3's matrix by feature) and "c5_shard" (one GPU's
          25 M-row shard of configs[4], implicit values), each with its epoch time, nnz/s and the
          roofline of its dominant kernel; "c3_load" (the data layer at full scale: C3 with scattered
          feature ids renumbered by frequency on the device by scd_renumber, then epochs on the result).
@@ -693,6 +693,47 @@ def leg_c4(args, ctx, d):
                                              for b in info["bins"]]}
 
 
+def leg_c2(args, ctx):
+    """configs[1]: synthetic sparse 100 k x 50 k with power-law lengths (~1% density), dual by example and
+    primal by feature on one GPU: epoch time, nnz/s and time to gap 1e-4 for each form."""
+    torch = ctx.torch
+    import synth
+    import paper_1702_07005_b200 as scd
+
+    cfg = synth.CONFIGS["C2"]
+    d = synth.gen_device(cfg)
+    N, M = d["n_rows"], d["n_cols"]
+    out = {"workload": "C2 (BASELINE configs[1]): 100000 x 50000 power-law rows, ~1% density, 1 GPU"}
+    for form in ("dual", "primal"):
+        if form == "dual":
+            p, i, v = d["ptr"], d["idx"], d["val"]
+        else:
+            p, i, v = scd.transpose(d["ptr"], d["idx"], d["val"], N, M, "csr")
+        s = scd.Solver(p, i, v, N, M, d["y"], cfg.lam, form, seed=2, profile=True)
+        stream = torch.cuda.ExternalStream(s.stream_handle)
+        info = s.info()
+        nnz = s.nnz
+        for t in range(1, 4):
+            s.epoch(t)
+        torch.cuda.synchronize()
+        s.profile_read()
+        steps = 20
+        l0 = s.info()["launches"]
+        el_ms = timed_epochs(ctx, s, stream, 4, steps, lambda t: s.epoch(t))
+        ctx.launches += s.info()["launches"] - l0
+        kprof = s.profile_read()
+        roof = kernel_roofline(s, info, kprof, BYTES_PER_NNZ, el_ms)
+        s.set_model(np.zeros(N if form == "dual" else M, np.float32))
+        ttg = time_to_gap(ctx, s, stream, lambda t: s.epoch(t), max_rounds=20)
+        s.close()
+        out[form] = {"nnz": nnz, "ms_per_step": el_ms / steps, "nnz_per_s": nnz * steps / (el_ms / 1e3),
+                     "roofline": roof, "time_to_gap": ttg,
+                     "schedule": [{k: b[k] for k in ("lanes", "count", "nnz", "grid", "head")} for b in info["bins"]]}
+    del d
+    torch.cuda.empty_cache()
+    return out
+
+
 def leg_c5(args, ctx):
     """configs[4]: criteo-shaped 200 M x 75 M one-hot, values implicit (val = NULL, NEXT-1), dual by
     example, 25 M rows per GPU (global N = 25 M x N: 200 M at N = 8).  N = 1: one shard's epoch (the
@@ -797,6 +838,11 @@ def main():
                 subs["c4_primal"] = leg_c4(args, ctx, d)
             except Exception as ex:
                 subs["c4_primal"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+            torch.cuda.empty_cache()
+            try:
+                subs["c2"] = leg_c2(args, ctx)
+            except Exception as ex:
+                subs["c2"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
             torch.cuda.empty_cache()
             try:
                 subs["c3_load"] = leg_load(args, ctx, d)
