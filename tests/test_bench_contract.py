@@ -45,3 +45,4 @@ def test_gpu_bench_json_line():
     assert d["time_to_gap"]["gap_trace"][-1] <= 1e-4
     assert d["c4_primal"]["ms_per_step"] > 0 and d["c5_shard"]["ms_per_step"] > 0
     assert all(d["c3_load"]["checks"].values()), d["c3_load"]
+    assert d["c2"]["dual"]["ms_per_step"] > 0 and d["c2"]["primal"]["time_to_gap"]["gap_trace"][-1] <= 1e-4
